@@ -1,0 +1,100 @@
+/*
+ * kvq.h -- C ABI of the B200 quantized paged-KV decode path
+ * (libkvq.so, built from paper_2605_29639_b200/csrc/ for sm_100a).
+ *
+ * This is the drop-in boundary.  Plain pointers, sizes and a CUDA stream
+ * handle passed as `void*` (a cudaStream_t / CUstream); no torch types.  The
+ * library never allocates, frees, synchronises or copies host<->device, so
+ * every entry point is stream-ordered and CUDA-graph capturable.  The caller
+ * owns every buffer, including the workspace.
+ *
+ * Reference interfaces replaced (arxiv/paper_2605_29639 / servesim; the
+ * reference models this path only as scalars):
+ *   kvq_quant_append   <- the GPU-tier KV write of an uncached suffix,
+ *                         simulator.py:384-396 (store.insert(h, GPU,
+ *                         _block_bytes(), ...)), sized by
+ *                         CostModel.kv_bytes_per_token, cost.py:41,73-74;
+ *                         semantics from PAPER.md:471-475.
+ *   kvq_decode_attn    <- CostModel.decode_step_us, cost.py:62-65, called
+ *                         from ClusterSim._decode_dur / _on_decode_step,
+ *                         simulator.py:499-517.
+ *   kvq_copy_blocks    <- the "partial block is exclusive" rule,
+ *                         tiered_cache.py:355-363 (copy-on-write of a shared
+ *                         partial tail block on fork).
+ *   kvq_page_bytes     <- ClusterSim._block_bytes, simulator.py:178-179.
+ *
+ * Error convention (mirrors the reference's ValueError / RuntimeError split,
+ * errors.py:6-33): 0 = ok; KVQ_EINVAL (shape / dtype / alignment);
+ * KVQ_EUNSUPPORTED (not sm_100, unknown kv dtype); KVQ_ECUDA (launch error).
+ * kvq_last_error() returns a thread-local message for the last failure.
+ */
+#ifndef KVQ_H
+#define KVQ_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define KVQ_ABI_VERSION 1
+#define KVQ_HEAD_DIM 128  /* d */
+#define KVQ_BLOCK_SIZE 16 /* tokens per page */
+#define KVQ_PAGE_BYTES 4224 /* one (block, kv head): 2x16x128 codes + 2x16 fp32 scales */
+
+enum kvq_status { KVQ_OK = 0, KVQ_EINVAL = -1, KVQ_EUNSUPPORTED = -2, KVQ_ECUDA = -3 };
+enum kvq_kv_dtype { KVQ_INT8 = 0, KVQ_FP8_E4M3 = 1 };
+enum kvq_out_dtype { KVQ_OUT_BF16 = 0, KVQ_OUT_F32 = 1 };
+enum kvq_out_layout { KVQ_OUT_BHD = 0 /* [B][Hq][d] */, KVQ_OUT_HBD = 1 /* [Hq][B][d] */ };
+
+int kvq_version(void);
+const char* kvq_last_error(void);
+size_t kvq_page_bytes(void);
+
+/* Quantize-on-append (K1).  k, v: bf16 [T][Hkv][128] with token strides
+ * k_token_stride / v_token_stride (in elements; head stride is 128, rows
+ * 8-byte aligned).  slot_mapping[t] = block * 16 + offset; slot < 0 skips
+ * token t.  pool: uint8 [num_blocks][Hkv][KVQ_PAGE_BYTES] (16-byte aligned).
+ * Per (token, head, K|V) row: amax -> scale = amax/QMAX -> codes
+ * (DESIGN.md §3), written into the page layout of DESIGN.md §2. */
+int kvq_quant_append(const void* k, const void* v, int64_t k_token_stride,
+                     int64_t v_token_stride, const int32_t* slot_mapping, int32_t T,
+                     int32_t Hkv, int32_t kv_dtype, void* pool, int64_t num_blocks,
+                     void* stream);
+
+/* Workspace for kvq_decode_attn: split partials (fp32 O + LSE) and the
+ * per-(sequence, kv head) arrival counters used by the fused split-KV
+ * combine.  The counter region must be zero the first time a workspace is
+ * used; the kernel leaves it zero again (graph-replay safe). */
+size_t kvq_decode_workspace_bytes(int32_t B, int32_t Hq, int32_t Hkv, int32_t max_splits);
+
+/* Split-KV geometry: pages per split chosen for a workload of `B` sequences,
+ * `Hkv` kv heads and `total_pages` pages summed over sequences (pass
+ * B * max_blocks when only the bound is known).  Returns pages_per_split >= 1;
+ * max_splits = ceil(max_blocks / pages_per_split). */
+int32_t kvq_decode_pages_per_split(int32_t B, int32_t Hkv, int64_t total_pages,
+                                   int32_t max_blocks);
+
+/* Paged GQA decode attention (K2 + fused split-KV combine).
+ *   q:           bf16 [B][Hq][128], batch stride q_batch_stride (elements)
+ *   pool:        uint8 [num_blocks][Hkv][KVQ_PAGE_BYTES]
+ *   block_table: int32 [B][max_blocks]; seq_lens: int32 [B] (<= 16*max_blocks)
+ *   sm_scale:    softmax scale (typically 1/sqrt(128))
+ *   out:         bf16 or fp32, layout per out_layout
+ * Hq % Hkv == 0 and Hq / Hkv <= 16.  seq_lens[b] == 0 yields zeros. */
+int kvq_decode_attn(const void* q, int64_t q_batch_stride, const void* pool, int64_t num_blocks,
+                    const int32_t* block_table, int32_t max_blocks, const int32_t* seq_lens,
+                    int32_t B, int32_t Hq, int32_t Hkv, int32_t kv_dtype, float sm_scale,
+                    int32_t pages_per_split, void* workspace, size_t workspace_bytes, void* out,
+                    int32_t out_dtype, int32_t out_layout, void* stream);
+
+/* Copy whole pages (all kv heads of a block): pairs[2*i] = src block,
+ * pairs[2*i+1] = dst block (device int32). */
+int kvq_copy_blocks(void* pool, int64_t num_blocks, int32_t Hkv, const int32_t* pairs,
+                    int32_t n_pairs, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* KVQ_H */

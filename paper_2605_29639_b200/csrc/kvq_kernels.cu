@@ -1,0 +1,869 @@
+// kvq_kernels.cu -- sm_100a kernels for the quantized paged-KV decode path and
+// the C ABI declared in include/kvq.h.
+//
+//   K1 quant_append_kernel   bf16 K/V rows -> per-(token, head) scale + 8-bit
+//                            codes scattered into the paged pool.
+//   K2 decode_kernel         warp-specialised paged GQA decode attention:
+//                            1 producer warp streams 4224-byte pages with
+//                            cp.async.bulk (TMA bulk copy) into an mbarrier
+//                            ring; 4 consumer warps dequantise in registers
+//                            and run QK^T / PV on the tensor cores
+//                            (mma.sync m16n8k16 f16 -> f32), online softmax,
+//                            fused split-KV combine by the last CTA.
+//   K3 copy_blocks_kernel    page copies for copy-on-write of shared tails.
+//
+// Layouts and the rounding contract: DESIGN.md §2-§3.  The CPU restatement
+// lives in oracle/ (tests only).
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+
+#include "kvq.h"
+
+namespace kvq {
+
+constexpr int HD = 128;
+constexpr int BS = 16;
+constexpr int PAGE = KVQ_PAGE_BYTES;
+constexpr int V_OFF = 2048;
+constexpr int KS_OFF = 4096;
+constexpr int VS_OFF = 4160;
+constexpr unsigned FULL = 0xffffffffu;
+
+// ---------------------------------------------------------------------------
+// Page layout helpers.
+// ---------------------------------------------------------------------------
+__host__ __device__ __forceinline__ int k_code_off(int tok, int d) {
+  const int j = d >> 4;
+  return tok * 128 + ((j ^ ((tok & 1) << 2)) << 4) + (d & 15);
+}
+__host__ __device__ __forceinline__ int v_code_off(int tok, int d) {
+  const int L = 2 * d + (tok & 1);
+  const int R = 2 * (tok >> 1) + (L >> 7);
+  const int l = L & 127;
+  return V_OFF + R * 128 + (((l >> 4) ^ (R & 7)) << 4) + (l & 15);
+}
+
+// ---------------------------------------------------------------------------
+// K1: quantize-on-append.  One warp per (token, kv head, K|V) row of 128.
+// ---------------------------------------------------------------------------
+template <int KVD>
+__global__ void __launch_bounds__(256) quant_append_kernel(
+    const __nv_bfloat16* __restrict__ k, const __nv_bfloat16* __restrict__ v, int64_t k_stride,
+    int64_t v_stride, const int32_t* __restrict__ slots, int T, int Hkv,
+    uint8_t* __restrict__ pool, int64_t num_blocks) {
+  const int64_t row = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= (int64_t)T * Hkv * 2) return;
+  const int kv = (int)(row & 1);
+  const int64_t th = row >> 1;
+  const int t = (int)(th / Hkv), h = (int)(th % Hkv);
+  const int slot = __ldg(slots + t);
+  if (slot < 0) return;
+  const int64_t blk = slot >> 4;
+  const int tok = slot & 15;
+  if (blk >= num_blocks) return;
+  const __nv_bfloat16* src =
+      (kv ? v + (int64_t)t * v_stride : k + (int64_t)t * k_stride) + h * HD + lane * 4;
+  const uint2 raw = __ldg(reinterpret_cast<const uint2*>(src));
+  float x[4];
+  x[0] = __uint_as_float(raw.x << 16);
+  x[1] = __uint_as_float(raw.x & 0xffff0000u);
+  x[2] = __uint_as_float(raw.y << 16);
+  x[3] = __uint_as_float(raw.y & 0xffff0000u);
+  float a = fmaxf(fmaxf(fabsf(x[0]), fabsf(x[1])), fmaxf(fabsf(x[2]), fabsf(x[3])));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) a = fmaxf(a, __shfl_xor_sync(FULL, a, o));
+  const float qmax = KVD == KVQ_FP8_E4M3 ? 448.0f : 127.0f;
+  // Contract: IEEE divisions, one RN multiply, no contraction.
+  const float scale = __fdiv_rn(a, qmax);
+  const float inv = a > 0.0f ? __fdiv_rn(qmax, a) : 0.0f;
+  float y[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) y[i] = __fmul_rn(x[i], inv);
+  uint32_t word;
+  if constexpr (KVD == KVQ_FP8_E4M3) {
+    uint16_t lo, hi;
+    asm("cvt.rn.satfinite.e4m3x2.f32 %0, %1, %2;" : "=h"(lo) : "f"(y[1]), "f"(y[0]));
+    asm("cvt.rn.satfinite.e4m3x2.f32 %0, %1, %2;" : "=h"(hi) : "f"(y[3]), "f"(y[2]));
+    word = (uint32_t)lo | ((uint32_t)hi << 16);
+  } else {
+    word = 0;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      int c = __float2int_rn(y[i]);  // cvt.rni.s32.f32: NaN -> 0, saturating
+      c = max(-127, min(127, c));
+      word |= ((uint32_t)(c & 0xff)) << (8 * i);
+    }
+  }
+  uint8_t* page = pool + ((int64_t)blk * Hkv + h) * PAGE;
+  if (kv == 0) {
+    *reinterpret_cast<uint32_t*>(page + k_code_off(tok, lane * 4)) = word;
+  } else {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) page[v_code_off(tok, lane * 4 + i)] = (uint8_t)(word >> (8 * i));
+  }
+  if (lane == 0) *reinterpret_cast<float*>(page + (kv ? VS_OFF : KS_OFF) + 4 * tok) = scale;
+}
+
+// ---------------------------------------------------------------------------
+// PTX helpers: shared-memory addresses, mbarriers, bulk async copy, MMA.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "KVQ_WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra KVQ_WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
+                                         uint64_t* bar, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1], %2, [%3], %4;" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint4 lds128(const uint8_t* p) {
+  uint4 r;
+  asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "r"(smem_u32(p)));
+  return r;
+}
+__device__ __forceinline__ float2 lds64f(const uint8_t* p) {
+  float2 r;
+  asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(r.x), "=f"(r.y) : "r"(smem_u32(p)));
+  return r;
+}
+__device__ __forceinline__ void mma16816(float (&c)[4], uint32_t a0, uint32_t a1, uint32_t a2,
+                                         uint32_t a3, uint32_t b0, uint32_t b1) {
+  asm(
+      "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+      "{%8,%9}, {%0,%1,%2,%3};"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ uint32_t pack_half2(float lo, float hi) {
+  __half2 h = __floats2half2_rn(lo, hi);
+  return *reinterpret_cast<uint32_t*>(&h);
+}
+// Exact 2^k for integer k (clamped to the normal fp32 range).
+__device__ __forceinline__ float pow2i(int k) {
+  k = max(-126, min(127, k));
+  return __int_as_float((127 + k) << 23);
+}
+__device__ __forceinline__ float fast_exp2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+// 8-bit codes -> two f16x2 registers (exact for every INT8 / E4M3 code).
+// Input bytes (b0, b1, b2, b3) -> lo = (b0, b1), hi = (b2, b3).
+template <int KVD>
+__device__ __forceinline__ void codes_to_f16x2(uint32_t w, uint32_t& lo, uint32_t& hi) {
+  if constexpr (KVD == KVQ_FP8_E4M3) {
+    asm("{\n\t.reg .b16 l, h;\n\tmov.b32 {l, h}, %2;\n\t"
+        "cvt.rn.f16x2.e4m3x2 %0, l;\n\tcvt.rn.f16x2.e4m3x2 %1, h;\n}"
+        : "=r"(lo), "=r"(hi)
+        : "r"(w));
+  } else {
+    // Offset-binary magic: fp16(0x64XX) = 1024 + XX; XX = code ^ 0x80 = code + 128.
+    const uint32_t u = w ^ 0x80808080u;
+    asm("prmt.b32 %0, %1, %2, 0x7170;" : "=r"(lo) : "r"(u), "r"(0x64646464u));
+    asm("prmt.b32 %0, %1, %2, 0x7372;" : "=r"(hi) : "r"(u), "r"(0x64646464u));
+    const uint32_t magic = 0x64806480u;  // (1152, 1152)
+    asm("sub.f16x2 %0, %0, %1;" : "+r"(lo) : "r"(magic));
+    asm("sub.f16x2 %0, %0, %1;" : "+r"(hi) : "r"(magic));
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K2: paged decode attention.
+// ---------------------------------------------------------------------------
+struct DecodeParams {
+  const __nv_bfloat16* q;
+  int64_t q_stride_b;
+  const uint8_t* pool;
+  int64_t num_blocks;
+  const int32_t* block_table;
+  int max_blocks;
+  const int32_t* seq_lens;
+  int B, Hq, Hkv, g;
+  float sm_scale_log2;  // sm_scale * log2(e)
+  int pages_per_split, max_splits;
+  float* part_o;    // [B*Hq][max_splits][128]
+  float* part_lse;  // [B*Hq][max_splits]   (log2 units)
+  int* counters;    // [B*Hkv]
+  void* out;
+  int out_f32, out_hbd;
+};
+
+constexpr int NW = 4;      // warps per CTA; every warp streams its own pages
+constexpr int S = 4;       // ring slots per warp (pages in flight per warp)
+constexpr int THREADS = 32 * NW;
+constexpr int CTAS_PER_SM = 3;
+constexpr size_t DECODE_SMEM = (size_t)NW * S * PAGE + NW * S * sizeof(uint64_t) + 16;
+static_assert((size_t)NW * S * PAGE >= (size_t)NW * 16 * HD * 4 + 2 * NW * 16 * 4,
+              "merge scratch must fit in the ring");
+
+__device__ __forceinline__ void store_out(const DecodeParams& p, int b, int head, int d0,
+                                          const float* vals) {
+  // 8 contiguous values starting at d0 for (b, head).
+  const int64_t row = p.out_hbd ? ((int64_t)head * p.B + b) : ((int64_t)b * p.Hq + head);
+  if (p.out_f32) {
+    float* o = reinterpret_cast<float*>(p.out) + row * HD + d0;
+    *reinterpret_cast<float4*>(o) = make_float4(vals[0], vals[1], vals[2], vals[3]);
+    *reinterpret_cast<float4*>(o + 4) = make_float4(vals[4], vals[5], vals[6], vals[7]);
+  } else {
+    __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(p.out) + row * HD + d0;
+    uint4 w;
+    __nv_bfloat162 t0 = __floats2bfloat162_rn(vals[0], vals[1]);
+    __nv_bfloat162 t1 = __floats2bfloat162_rn(vals[2], vals[3]);
+    __nv_bfloat162 t2 = __floats2bfloat162_rn(vals[4], vals[5]);
+    __nv_bfloat162 t3 = __floats2bfloat162_rn(vals[6], vals[7]);
+    w.x = *reinterpret_cast<uint32_t*>(&t0);
+    w.y = *reinterpret_cast<uint32_t*>(&t1);
+    w.z = *reinterpret_cast<uint32_t*>(&t2);
+    w.w = *reinterpret_cast<uint32_t*>(&t3);
+    *reinterpret_cast<uint4*>(o) = w;
+  }
+}
+
+// Per-warp page stream: warp w of the CTA owns pages w, w + NW, w + 2NW, ...
+// of the split; page j of the warp lands in slot j % S of the warp's ring.
+struct PageStream {
+  const int32_t* bt;       // block table row, offset to the split's first page
+  const uint8_t* head_base;
+  int64_t blk_stride;
+  int64_t num_blocks;
+  int warp, nj;            // nj = pages this warp processes
+  uint8_t* ring;           // this warp's S slots
+  uint64_t* full;          // this warp's S barriers
+  uint64_t policy;
+  int cur, nxt;            // block ids of pages [base, base+32) and [base+32, base+64) (lane-parallel)
+  int base;
+
+  __device__ __forceinline__ int load_ids(int j0, int lane) const {
+    const int j = j0 + lane;
+    int blk = j < nj ? __ldg(bt + warp + j * NW) : 0;
+    if ((unsigned)blk >= (unsigned long long)num_blocks) blk = 0;
+    return blk;
+  }
+  __device__ __forceinline__ void init(int lane) {
+    base = 0;
+    cur = load_ids(0, lane);
+    nxt = load_ids(32, lane);
+  }
+  // Issue the bulk copy of page j (j >= base, all lanes participate).
+  __device__ __forceinline__ void issue(int j, int lane) {
+    if (j >= base + 32) {  // advance the id window (warp-uniform)
+      base += 32;
+      cur = nxt;
+      nxt = load_ids(base + 32, lane);
+    }
+    const int blk = __shfl_sync(FULL, cur, j - base);
+    if (lane == 0) {
+      const int s = j % S;
+      mbar_arrive_expect_tx(&full[s], PAGE);
+      bulk_g2s(ring + s * PAGE, head_base + blk * blk_stride, PAGE, &full[s], policy);
+    }
+  }
+};
+
+template <int KVD, bool HI>
+__global__ void __launch_bounds__(THREADS, CTAS_PER_SM) decode_kernel(const DecodeParams p) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + NW * S * PAGE);
+  int* flag = reinterpret_cast<int*>(bars + NW * S);
+
+  const int split = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
+  const int g = p.g;
+  const int L = min(__ldg(p.seq_lens + b), p.max_blocks * BS);
+  const int npages = (L + BS - 1) / BS;
+  const int nsplit = max(1, (npages + p.pages_per_split - 1) / p.pages_per_split);
+  if (split >= nsplit) return;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  if (L <= 0) {  // empty sequence: zeros, nothing to combine
+    const float z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    for (int idx = threadIdx.x; idx < g * (HD / 8); idx += THREADS)
+      store_out(p, b, h * g + idx / (HD / 8), (idx % (HD / 8)) * 8, z);
+    return;
+  }
+  const int pg0 = split * p.pages_per_split;
+  const int n = min(npages, pg0 + p.pages_per_split) - pg0;
+
+  PageStream ps;
+  ps.bt = p.block_table + (int64_t)b * p.max_blocks + pg0;
+  ps.head_base = p.pool + (int64_t)h * PAGE;
+  ps.blk_stride = (int64_t)p.Hkv * PAGE;
+  ps.num_blocks = p.num_blocks;
+  ps.warp = warp;
+  ps.nj = n > warp ? (n - warp + NW - 1) / NW : 0;
+  ps.ring = smem + warp * S * PAGE;
+  ps.full = bars + warp * S;
+  ps.policy = policy_evict_first();
+  if (lane == 0) {
+#pragma unroll
+    for (int s = 0; s < S; ++s) mbar_init(&ps.full[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+  ps.init(lane);
+#pragma unroll 1
+  for (int j = 0; j < S && j < ps.nj; ++j) ps.issue(j, lane);
+
+  const int r = lane >> 2, cc = lane & 3;
+  const bool row_lo_valid = r < g;
+  const bool row_hi_valid = HI && (r + 8 < g);
+
+  // Q fragments: head row r (and r + 8), d ranges [16cc, 16cc+16) and [64+16cc, +16).
+  // k-step i covers d = base(i) + {0,1} (a0/a1) and base(i) + {2,3} (a2/a3),
+  // base(i) = (i < 4 ? 16cc + 4i : 64 + 16cc + 4(i-4)).
+  uint32_t qlo[8][2], qhi[8][2];
+  float qscale;
+  {
+    const __nv_bfloat16* qrow = p.q + (int64_t)b * p.q_stride_b + (int64_t)(h * g) * HD;
+    uint4 raw[2][4];
+#pragma unroll
+    for (int rr = 0; rr < 2; ++rr) {
+      const bool valid = rr == 0 ? row_lo_valid : row_hi_valid;
+      const __nv_bfloat16* src = qrow + (r + 8 * rr) * HD;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int d = (u < 2 ? 16 * cc + 8 * u : 64 + 16 * cc + 8 * (u - 2));
+        raw[rr][u] = valid ? __ldg(reinterpret_cast<const uint4*>(src + d)) : make_uint4(0, 0, 0, 0);
+      }
+    }
+    float amax = 0.0f;
+#pragma unroll
+    for (int rr = 0; rr < 2; ++rr)
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const uint32_t w[4] = {raw[rr][u].x, raw[rr][u].y, raw[rr][u].z, raw[rr][u].w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          amax = fmaxf(amax, fabsf(__uint_as_float(w[e] << 16)));
+          amax = fmaxf(amax, fabsf(__uint_as_float(w[e] & 0xffff0000u)));
+        }
+      }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) amax = fmaxf(amax, __shfl_xor_sync(FULL, amax, o));
+    // Exact power-of-two prescale so max|q'| < 2^14 (fp16-safe); undone in qscale.
+    int ex = 0;
+    if (amax > 0.0f) frexpf(amax, &ex);
+    const float pre = pow2i(14 - ex);
+    qscale = p.sm_scale_log2 / pre;
+#pragma unroll
+    for (int rr = 0; rr < 2; ++rr)
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const uint32_t w[4] = {raw[rr][u].x, raw[rr][u].y, raw[rr][u].z, raw[rr][u].w};
+        uint32_t hw[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+          hw[e] = pack_half2(__uint_as_float(w[e] << 16) * pre,
+                             __uint_as_float(w[e] & 0xffff0000u) * pre);
+        const int i0 = 2 * u;  // uint4 u holds d = base(i0) .. base(i0) + 7
+        uint32_t(&dst)[8][2] = rr == 0 ? qlo : qhi;
+        dst[i0][0] = hw[0];
+        dst[i0][1] = hw[1];
+        dst[i0 + 1][0] = hw[2];
+        dst[i0 + 1][1] = hw[3];
+      }
+  }
+
+  // Per-thread smem offsets inside a page (fixed for every page).
+  const int koff0 = r * 128 + ((cc ^ ((r & 1) << 2)) << 4);
+  const int koff1 = r * 128 + (((cc + 4) ^ ((r & 1) << 2)) << 4);
+  const int koff2 = koff0 + 8 * 128;  // row r+8 (same parity)
+  const int koff3 = koff1 + 8 * 128;
+  const int R0 = 2 * cc, R1 = 2 * cc + 1;
+  const int voff0 = V_OFF + R0 * 128 + ((r ^ (R0 & 7)) << 4);        // tokens 2cc,2cc+1  d in [8r, 8r+8)
+  const int voff1 = V_OFF + R1 * 128 + ((r ^ (R1 & 7)) << 4);        // d in [64+8r, ...)
+  const int voff2 = V_OFF + (R0 + 8) * 128 + ((r ^ (R0 & 7)) << 4);  // tokens 8+2cc, 9+2cc
+  const int voff3 = V_OFF + (R1 + 8) * 128 + ((r ^ (R1 & 7)) << 4);
+
+  float o[16][4];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.0f;
+  float m_lo = -INFINITY, m_hi = -INFINITY, l_lo = 0.0f, l_hi = 0.0f;
+  float escale = 1.0f;  // V-scale normaliser 2^E (fp16 range guard for P')
+  bool escale_set = false;
+
+#pragma unroll 1
+  for (int j = 0; j < ps.nj; ++j) {
+    const int s = j % S;
+    mbar_wait(&ps.full[s], (j / S) & 1);
+    const uint8_t* pg = ps.ring + s * PAGE;
+    const uint4 k0 = lds128(pg + koff0), k1 = lds128(pg + koff1);
+    const uint4 k2 = lds128(pg + koff2), k3 = lds128(pg + koff3);
+    const uint4 v0 = lds128(pg + voff0), v1 = lds128(pg + voff1);
+    const uint4 v2 = lds128(pg + voff2), v3 = lds128(pg + voff3);
+    const float2 ks0 = lds64f(pg + KS_OFF + 8 * cc), ks1 = lds64f(pg + KS_OFF + 32 + 8 * cc);
+    float2 vs0 = lds64f(pg + VS_OFF + 8 * cc), vs1 = lds64f(pg + VS_OFF + 32 + 8 * cc);
+
+    // ---- S^T tile: rows = heads (r, r+8), cols = tokens (n-tile 0: 0..7, 1: 8..15);
+    //      two accumulator sets per n-tile halve the dependent-MMA chain.
+    float sc[2][4], sd[2][4];
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) sc[nt][e] = sd[nt][e] = 0.0f;
+    {
+      const uint32_t kw[2][8] = {{k0.x, k0.y, k0.z, k0.w, k1.x, k1.y, k1.z, k1.w},
+                                 {k2.x, k2.y, k2.z, k2.w, k3.x, k3.y, k3.z, k3.w}};
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt) {
+          uint32_t b0, b1;
+          codes_to_f16x2<KVD>(kw[nt][i], b0, b1);
+          mma16816(i < 4 ? sc[nt] : sd[nt], qlo[i][0], HI ? qhi[i][0] : 0u, qlo[i][1],
+                   HI ? qhi[i][1] : 0u, b0, b1);
+        }
+    }
+    // ---- scores (log2 units) + masking of the tail page
+    const int tok_base = (pg0 + warp + j * NW) * BS;
+    const bool tail = tok_base + BS > L;
+    const float kscl[4] = {ks0.x * qscale, ks0.y * qscale, ks1.x * qscale, ks1.y * qscale};
+    float s_lo[4] = {(sc[0][0] + sd[0][0]) * kscl[0], (sc[0][1] + sd[0][1]) * kscl[1],
+                     (sc[1][0] + sd[1][0]) * kscl[2], (sc[1][1] + sd[1][1]) * kscl[3]};
+    float s_hi[4] = {(sc[0][2] + sd[0][2]) * kscl[0], (sc[0][3] + sd[0][3]) * kscl[1],
+                     (sc[1][2] + sd[1][2]) * kscl[2], (sc[1][3] + sd[1][3]) * kscl[3]};
+    if (tail) {
+      const int tk[4] = {2 * cc, 2 * cc + 1, 8 + 2 * cc, 9 + 2 * cc};
+#pragma unroll
+      for (int e = 0; e < 4; ++e)
+        if (tok_base + tk[e] >= L) {
+          s_lo[e] = -INFINITY;
+          s_hi[e] = -INFINITY;
+        }
+      if (tok_base + 2 * cc >= L) vs0.x = 0.0f;
+      if (tok_base + 2 * cc + 1 >= L) vs0.y = 0.0f;
+      if (tok_base + 8 + 2 * cc >= L) vs1.x = 0.0f;
+      if (tok_base + 9 + 2 * cc >= L) vs1.y = 0.0f;
+    }
+    if (!row_lo_valid) s_lo[0] = s_lo[1] = s_lo[2] = s_lo[3] = 0.0f;
+    if (!row_hi_valid) s_hi[0] = s_hi[1] = s_hi[2] = s_hi[3] = 0.0f;
+    float mx_lo = fmaxf(fmaxf(s_lo[0], s_lo[1]), fmaxf(s_lo[2], s_lo[3]));
+    float mx_hi = fmaxf(fmaxf(s_hi[0], s_hi[1]), fmaxf(s_hi[2], s_hi[3]));
+    float vmax = fmaxf(fmaxf(vs0.x, vs0.y), fmaxf(vs1.x, vs1.y));
+#pragma unroll
+    for (int o2 = 1; o2 <= 2; o2 <<= 1) {
+      mx_lo = fmaxf(mx_lo, __shfl_xor_sync(FULL, mx_lo, o2));
+      if (HI) mx_hi = fmaxf(mx_hi, __shfl_xor_sync(FULL, mx_hi, o2));
+      vmax = fmaxf(vmax, __shfl_xor_sync(FULL, vmax, o2));
+    }
+    // ---- lazy rescale (threshold 2^8 for p, [2^-10, 2^4] for the V normaliser)
+    const bool need_lo = row_lo_valid && mx_lo > m_lo + 8.0f;
+    const bool need_hi = row_hi_valid && mx_hi > m_hi + 8.0f;
+    const float ve = vmax * escale;
+    const bool need_e = vmax > 0.0f && (!escale_set || ve > 16.0f || ve < 0.0009765625f);
+    if (__any_sync(FULL, need_lo || need_hi || need_e)) {
+      float e_new = escale;
+      if (need_e) {
+        int ex;
+        frexpf(vmax, &ex);
+        e_new = pow2i(-ex);
+        escale_set = true;
+      }
+      const float er = e_new / escale;  // exact power of two
+      const float mn_lo = need_lo ? mx_lo : m_lo;
+      const float mn_hi = need_hi ? mx_hi : m_hi;
+      const float c_lo = need_lo ? fast_exp2(m_lo - mn_lo) : 1.0f;
+      const float c_hi = need_hi ? fast_exp2(m_hi - mn_hi) : 1.0f;
+      l_lo *= c_lo;
+      l_hi *= c_hi;
+      const float f_lo = c_lo * er, f_hi = c_hi * er;
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        o[i][0] *= f_lo;
+        o[i][1] *= f_lo;
+        if (HI) {
+          o[i][2] *= f_hi;
+          o[i][3] *= f_hi;
+        }
+      }
+      m_lo = mn_lo;
+      m_hi = mn_hi;
+      escale = e_new;
+    }
+    // ---- probabilities: p (fp32, for l) and P' = p * scale_v * 2^E (fp16, for PV)
+    const float w[4] = {vs0.x * escale, vs0.y * escale, vs1.x * escale, vs1.y * escale};
+    float p_lo[4], p_hi[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      p_lo[e] = row_lo_valid ? fast_exp2(s_lo[e] - m_lo) : 0.0f;
+      p_hi[e] = row_hi_valid ? fast_exp2(s_hi[e] - m_hi) : 0.0f;
+      l_lo += p_lo[e];
+      l_hi += p_hi[e];
+    }
+    const uint32_t pa0 = pack_half2(p_lo[0] * w[0], p_lo[1] * w[1]);
+    const uint32_t pa2 = pack_half2(p_lo[2] * w[2], p_lo[3] * w[3]);
+    const uint32_t pa1 = HI ? pack_half2(p_hi[0] * w[0], p_hi[1] * w[1]) : 0u;
+    const uint32_t pa3 = HI ? pack_half2(p_hi[2] * w[2], p_hi[3] * w[3]) : 0u;
+
+    // ---- O += P' V : n-tile nt <-> d = (nt < 8 ? 8r + nt : 64 + 8r + nt - 8) for B column r
+    const uint32_t vw[2][8] = {{v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w},
+                               {v2.x, v2.y, v2.z, v2.w, v3.x, v3.y, v3.z, v3.w}};
+    uint32_t vmask0 = 0xffffffffu, vmask1 = 0xffffffffu;
+    if (KVD == KVQ_FP8_E4M3 && tail) {  // garbage E4M3 codes may be NaN: zero masked tokens
+      vmask0 = (tok_base + 2 * cc < L ? 0x0000ffffu : 0u) | (tok_base + 2 * cc + 1 < L ? 0xffff0000u : 0u);
+      vmask1 = (tok_base + 8 + 2 * cc < L ? 0x0000ffffu : 0u) | (tok_base + 9 + 2 * cc < L ? 0xffff0000u : 0u);
+    }
+#pragma unroll
+    for (int jj = 0; jj < 8; ++jj) {
+      uint32_t b0a, b0b, b1a, b1b;
+      codes_to_f16x2<KVD>(vw[0][jj], b0a, b0b);
+      codes_to_f16x2<KVD>(vw[1][jj], b1a, b1b);
+      if (KVD == KVQ_FP8_E4M3) {
+        b0a &= vmask0;
+        b0b &= vmask0;
+        b1a &= vmask1;
+        b1b &= vmask1;
+      }
+      // word jj of a chunk -> d pair (2jj, 2jj+1) within its 8-wide d range -> n-tiles
+      const int nt0 = (jj < 4) ? 2 * jj : 8 + 2 * (jj - 4);
+      mma16816(o[nt0], pa0, pa1, pa2, pa3, b0a, b1a);
+      mma16816(o[nt0 + 1], pa0, pa1, pa2, pa3, b0b, b1b);
+    }
+    // ---- refill this slot with page j + S (its smem was fully consumed above)
+    if (j + S < ps.nj) {
+      __syncwarp();
+      if (lane == 0) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      ps.issue(j + S, lane);
+    }
+  }
+
+  // ===== CTA merge of the NW warps =====
+  l_lo += __shfl_xor_sync(FULL, l_lo, 1);
+  l_lo += __shfl_xor_sync(FULL, l_lo, 2);
+  l_hi += __shfl_xor_sync(FULL, l_hi, 1);
+  l_hi += __shfl_xor_sync(FULL, l_hi, 2);
+  __syncthreads();  // every ring slot consumed: reuse smem as merge scratch
+  float* so = reinterpret_cast<float*>(smem);  // [NW][16][128]
+  float* sm = so + NW * 16 * HD;               // [NW][16] m
+  float* sl = sm + NW * 16;                    // [NW][16] l
+  if (cc == 0) {
+    sm[warp * 16 + r] = row_lo_valid ? m_lo : -INFINITY;
+    sl[warp * 16 + r] = l_lo;
+    sm[warp * 16 + r + 8] = row_hi_valid ? m_hi : -INFINITY;
+    sl[warp * 16 + r + 8] = l_hi;
+  }
+  __syncthreads();
+  {
+    float M_lo = -INFINITY, M_hi = -INFINITY;
+#pragma unroll
+    for (int w2 = 0; w2 < NW; ++w2) {
+      M_lo = fmaxf(M_lo, sm[w2 * 16 + r]);
+      M_hi = fmaxf(M_hi, sm[w2 * 16 + r + 8]);
+    }
+    const float f_lo = (row_lo_valid && m_lo > -INFINITY) ? fast_exp2(m_lo - M_lo) / escale : 0.0f;
+    const float f_hi = (row_hi_valid && m_hi > -INFINITY) ? fast_exp2(m_hi - M_hi) / escale : 0.0f;
+    float* mine = so + warp * 16 * HD;
+#pragma unroll
+    for (int nt = 0; nt < 16; ++nt) {
+      const int d0 = (nt < 8 ? 16 * cc + nt : 64 + 16 * cc + (nt - 8));
+      mine[r * HD + d0] = o[nt][0] * f_lo;
+      mine[r * HD + d0 + 8] = o[nt][1] * f_lo;
+      if (HI) {
+        mine[(r + 8) * HD + d0] = o[nt][2] * f_hi;
+        mine[(r + 8) * HD + d0 + 8] = o[nt][3] * f_hi;
+      }
+    }
+  }
+  __syncthreads();
+  // Each thread finalises 8 contiguous d of one head row.
+  const int tid = threadIdx.x;
+  const int nrow_items = g * (HD / 8);
+  for (int item = tid; item < nrow_items; item += THREADS) {
+    const int row = item / (HD / 8), d0 = (item % (HD / 8)) * 8;
+    float M = -INFINITY;
+#pragma unroll
+    for (int w2 = 0; w2 < NW; ++w2) M = fmaxf(M, sm[w2 * 16 + row]);
+    float lsum = 0.0f;
+#pragma unroll
+    for (int w2 = 0; w2 < NW; ++w2) {
+      const float mw = sm[w2 * 16 + row];
+      if (mw > -INFINITY) lsum += sl[w2 * 16 + row] * fast_exp2(mw - M);
+    }
+    float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#pragma unroll
+    for (int w2 = 0; w2 < NW; ++w2) {
+      if (sm[w2 * 16 + row] == -INFINITY) continue;  // warp saw no page
+      const float* src = so + (w2 * 16 + row) * HD + d0;
+#pragma unroll
+      for (int e = 0; e < 8; ++e) acc[e] += src[e];
+    }
+    const float inv = 1.0f / lsum;
+#pragma unroll
+    for (int e = 0; e < 8; ++e) acc[e] *= inv;
+    const int head = h * g + row;
+    if (nsplit == 1) {
+      store_out(p, b, head, d0, acc);
+    } else {
+      float* dst = p.part_o + (((int64_t)b * p.Hq + head) * p.max_splits + split) * HD + d0;
+      *reinterpret_cast<float4*>(dst) = make_float4(acc[0], acc[1], acc[2], acc[3]);
+      *reinterpret_cast<float4*>(dst + 4) = make_float4(acc[4], acc[5], acc[6], acc[7]);
+      if (d0 == 0) p.part_lse[((int64_t)b * p.Hq + head) * p.max_splits + split] = M + __log2f(lsum);
+    }
+  }
+  if (nsplit == 1) return;
+
+  // ===== fused split-KV combine: the last CTA of (b, h) merges all splits =====
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) {
+    const int prev = atomicAdd(p.counters + (int64_t)b * p.Hkv + h, 1);
+    const int last = prev == nsplit - 1;
+    if (last) p.counters[(int64_t)b * p.Hkv + h] = 0;  // reset for the next launch / replay
+    *flag = last;
+  }
+  __syncthreads();
+  if (!*flag) return;
+  __threadfence();
+  for (int item = tid; item < nrow_items; item += THREADS) {
+    const int row = item / (HD / 8), d0 = (item % (HD / 8)) * 8;
+    const int head = h * g + row;
+    const int64_t base = ((int64_t)b * p.Hq + head) * p.max_splits;
+    float M = -INFINITY;
+    for (int sp = 0; sp < nsplit; ++sp) M = fmaxf(M, __ldcg(p.part_lse + base + sp));
+    float wsum = 0.0f, acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    for (int sp = 0; sp < nsplit; ++sp) {
+      const float wgt = fast_exp2(__ldcg(p.part_lse + base + sp) - M);
+      wsum += wgt;
+      const float4 a = __ldcg(reinterpret_cast<const float4*>(p.part_o + (base + sp) * HD + d0));
+      const float4 c = __ldcg(reinterpret_cast<const float4*>(p.part_o + (base + sp) * HD + d0 + 4));
+      acc[0] += wgt * a.x;
+      acc[1] += wgt * a.y;
+      acc[2] += wgt * a.z;
+      acc[3] += wgt * a.w;
+      acc[4] += wgt * c.x;
+      acc[5] += wgt * c.y;
+      acc[6] += wgt * c.z;
+      acc[7] += wgt * c.w;
+    }
+    const float inv = 1.0f / wsum;
+#pragma unroll
+    for (int e = 0; e < 8; ++e) acc[e] *= inv;
+    store_out(p, b, head, d0, acc);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K3: page copies for copy-on-write.
+// ---------------------------------------------------------------------------
+__global__ void copy_blocks_kernel(uint8_t* __restrict__ pool, int64_t num_blocks, int Hkv,
+                                   const int32_t* __restrict__ pairs) {
+  const int i = blockIdx.x;
+  const int src = __ldg(pairs + 2 * i), dst = __ldg(pairs + 2 * i + 1);
+  if ((unsigned)src >= (unsigned long long)num_blocks || (unsigned)dst >= (unsigned long long)num_blocks)
+    return;
+  const int64_t bytes = (int64_t)Hkv * PAGE;
+  const uint4* s = reinterpret_cast<const uint4*>(pool + src * bytes);
+  uint4* d = reinterpret_cast<uint4*>(pool + dst * bytes);
+  for (int64_t j = threadIdx.x; j < bytes / 16; j += blockDim.x) d[j] = s[j];
+}
+
+}  // namespace kvq
+
+// ===========================================================================
+// C ABI
+// ===========================================================================
+namespace {
+thread_local char g_err[512] = "";
+int fail(int code, const char* msg) {
+  snprintf(g_err, sizeof(g_err), "%s", msg);
+  return code;
+}
+int check_launch(const char* what) {
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    snprintf(g_err, sizeof(g_err), "%s: %s", what, cudaGetErrorString(e));
+    return KVQ_ECUDA;
+  }
+  return KVQ_OK;
+}
+int check_device() {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return fail(KVQ_ECUDA, "cudaGetDevice failed");
+  int major = 0, minor = 0;
+  cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+  cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev);
+  if (major != 10 || minor != 0) return fail(KVQ_EUNSUPPORTED, "libkvq is built for sm_100a (B200) only");
+  return KVQ_OK;
+}
+bool aligned(const void* p, size_t a) { return (reinterpret_cast<uintptr_t>(p) % a) == 0; }
+}  // namespace
+
+extern "C" {
+
+int kvq_version(void) { return KVQ_ABI_VERSION; }
+const char* kvq_last_error(void) { return g_err; }
+size_t kvq_page_bytes(void) { return KVQ_PAGE_BYTES; }
+
+int kvq_quant_append(const void* k, const void* v, int64_t k_token_stride, int64_t v_token_stride,
+                     const int32_t* slot_mapping, int32_t T, int32_t Hkv, int32_t kv_dtype,
+                     void* pool, int64_t num_blocks, void* stream) {
+  if (T < 0 || Hkv <= 0 || num_blocks <= 0) return fail(KVQ_EINVAL, "quant_append: bad sizes");
+  if (T == 0) return KVQ_OK;
+  if (!k || !v || !slot_mapping || !pool) return fail(KVQ_EINVAL, "quant_append: null pointer");
+  if (!aligned(k, 8) || !aligned(v, 8) || !aligned(pool, 16) || (k_token_stride % 4) || (v_token_stride % 4))
+    return fail(KVQ_EINVAL, "quant_append: k/v rows must be 8-byte aligned, pool 16-byte aligned");
+  if (kv_dtype != KVQ_INT8 && kv_dtype != KVQ_FP8_E4M3)
+    return fail(KVQ_EUNSUPPORTED, "quant_append: unknown kv dtype");
+  if (int rc = check_device()) return rc;
+  const int64_t rows = (int64_t)T * Hkv * 2;
+  const dim3 grid((unsigned)((rows + 7) / 8));
+  auto st = static_cast<cudaStream_t>(stream);
+  if (kv_dtype == KVQ_INT8)
+    kvq::quant_append_kernel<KVQ_INT8><<<grid, 256, 0, st>>>(
+        static_cast<const __nv_bfloat16*>(k), static_cast<const __nv_bfloat16*>(v), k_token_stride,
+        v_token_stride, slot_mapping, T, Hkv, static_cast<uint8_t*>(pool), num_blocks);
+  else
+    kvq::quant_append_kernel<KVQ_FP8_E4M3><<<grid, 256, 0, st>>>(
+        static_cast<const __nv_bfloat16*>(k), static_cast<const __nv_bfloat16*>(v), k_token_stride,
+        v_token_stride, slot_mapping, T, Hkv, static_cast<uint8_t*>(pool), num_blocks);
+  return check_launch("quant_append");
+}
+
+size_t kvq_decode_workspace_bytes(int32_t B, int32_t Hq, int32_t Hkv, int32_t max_splits) {
+  const size_t po = (size_t)B * Hq * max_splits * KVQ_HEAD_DIM * sizeof(float);
+  const size_t pl = (size_t)B * Hq * max_splits * sizeof(float);
+  const size_t cnt = (size_t)B * Hkv * sizeof(int);
+  auto up = [](size_t x) { return (x + 255) & ~(size_t)255; };
+  return up(cnt) + up(po) + up(pl);
+}
+
+int32_t kvq_decode_pages_per_split(int32_t B, int32_t Hkv, int64_t total_pages, int32_t max_blocks) {
+  // Uniform splits of <= 64 pages (270 KB of KV per CTA) so the ragged tail is
+  // at most one short CTA; as few waves of CTAs_PER_SM x SMs as that allows.
+  (void)B;
+  int sms = 148, dev = 0;
+  if (cudaGetDevice(&dev) == cudaSuccess) {
+    int v = 0;
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess && v > 0) sms = v;
+  } else {
+    cudaGetLastError();
+  }
+  const int64_t slots = (int64_t)sms * kvq::CTAS_PER_SM;
+  const int64_t work = total_pages * (int64_t)Hkv;
+  const int64_t waves = (work + slots * 64 - 1) / (slots * 64);
+  int64_t pps = (work + slots * (waves > 0 ? waves : 1) - 1) / (slots * (waves > 0 ? waves : 1));
+  if (pps < 8) pps = 8;
+  if (pps > 64) pps = 64;
+  if (max_blocks > 0 && pps > max_blocks) pps = max_blocks;
+  return (int32_t)(pps > 0 ? pps : 1);
+}
+
+int kvq_decode_attn(const void* q, int64_t q_batch_stride, const void* pool, int64_t num_blocks,
+                    const int32_t* block_table, int32_t max_blocks, const int32_t* seq_lens,
+                    int32_t B, int32_t Hq, int32_t Hkv, int32_t kv_dtype, float sm_scale,
+                    int32_t pages_per_split, void* workspace, size_t workspace_bytes, void* out,
+                    int32_t out_dtype, int32_t out_layout, void* stream) {
+  if (B < 0 || Hq <= 0 || Hkv <= 0 || max_blocks <= 0 || num_blocks <= 0)
+    return fail(KVQ_EINVAL, "decode_attn: bad sizes");
+  if (B == 0) return KVQ_OK;
+  if (Hq % Hkv != 0 || Hq / Hkv > 16)
+    return fail(KVQ_EINVAL, "decode_attn: need Hq % Hkv == 0 and Hq / Hkv <= 16");
+  if (!q || !pool || !block_table || !seq_lens || !out || !workspace)
+    return fail(KVQ_EINVAL, "decode_attn: null pointer");
+  if (!aligned(q, 16) || (q_batch_stride % 8) || !aligned(pool, 16) || !aligned(out, 16) ||
+      !aligned(workspace, 256))
+    return fail(KVQ_EINVAL, "decode_attn: q/pool/out must be 16-byte aligned, workspace 256-byte");
+  if (kv_dtype != KVQ_INT8 && kv_dtype != KVQ_FP8_E4M3)
+    return fail(KVQ_EUNSUPPORTED, "decode_attn: unknown kv dtype");
+  if (out_dtype != KVQ_OUT_BF16 && out_dtype != KVQ_OUT_F32)
+    return fail(KVQ_EINVAL, "decode_attn: bad out dtype");
+  if (out_layout != KVQ_OUT_BHD && out_layout != KVQ_OUT_HBD)
+    return fail(KVQ_EINVAL, "decode_attn: bad out layout");
+  if (pages_per_split <= 0)
+    pages_per_split = kvq_decode_pages_per_split(B, Hkv, (int64_t)B * max_blocks, max_blocks);
+  const int max_splits = (max_blocks + pages_per_split - 1) / pages_per_split;
+  if (workspace_bytes < kvq_decode_workspace_bytes(B, Hq, Hkv, max_splits))
+    return fail(KVQ_EINVAL, "decode_attn: workspace too small");
+  if (int rc = check_device()) return rc;
+
+  auto up = [](size_t x) { return (x + 255) & ~(size_t)255; };
+  uint8_t* ws = static_cast<uint8_t*>(workspace);
+  kvq::DecodeParams prm;
+  prm.q = static_cast<const __nv_bfloat16*>(q);
+  prm.q_stride_b = q_batch_stride;
+  prm.pool = static_cast<const uint8_t*>(pool);
+  prm.num_blocks = num_blocks;
+  prm.block_table = block_table;
+  prm.max_blocks = max_blocks;
+  prm.seq_lens = seq_lens;
+  prm.B = B;
+  prm.Hq = Hq;
+  prm.Hkv = Hkv;
+  prm.g = Hq / Hkv;
+  prm.sm_scale_log2 = sm_scale * 1.4426950408889634f;
+  prm.pages_per_split = pages_per_split;
+  prm.max_splits = max_splits;
+  prm.counters = reinterpret_cast<int*>(ws);
+  prm.part_o = reinterpret_cast<float*>(ws + up((size_t)B * Hkv * sizeof(int)));
+  prm.part_lse = reinterpret_cast<float*>(ws + up((size_t)B * Hkv * sizeof(int)) +
+                                          up((size_t)B * Hq * max_splits * KVQ_HEAD_DIM * sizeof(float)));
+  prm.out = out;
+  prm.out_f32 = out_dtype == KVQ_OUT_F32;
+  prm.out_hbd = out_layout == KVQ_OUT_HBD;
+
+  const dim3 grid((unsigned)max_splits, (unsigned)Hkv, (unsigned)B);
+  auto st = static_cast<cudaStream_t>(stream);
+  const bool hi = prm.g > 8;
+  auto launch = [&](auto kernel) -> int {
+    cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)kvq::DECODE_SMEM);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
+                               cudaSharedmemCarveoutMaxShared);
+    if (e != cudaSuccess) return fail(KVQ_ECUDA, cudaGetErrorString(e));
+    kernel<<<grid, kvq::THREADS, kvq::DECODE_SMEM, st>>>(prm);
+    return check_launch("decode_attn");
+  };
+  if (kv_dtype == KVQ_INT8)
+    return hi ? launch(kvq::decode_kernel<KVQ_INT8, true>) : launch(kvq::decode_kernel<KVQ_INT8, false>);
+  return hi ? launch(kvq::decode_kernel<KVQ_FP8_E4M3, true>)
+            : launch(kvq::decode_kernel<KVQ_FP8_E4M3, false>);
+}
+
+int kvq_copy_blocks(void* pool, int64_t num_blocks, int32_t Hkv, const int32_t* pairs,
+                    int32_t n_pairs, void* stream) {
+  if (n_pairs < 0 || Hkv <= 0 || num_blocks <= 0) return fail(KVQ_EINVAL, "copy_blocks: bad sizes");
+  if (n_pairs == 0) return KVQ_OK;
+  if (!pool || !pairs) return fail(KVQ_EINVAL, "copy_blocks: null pointer");
+  if (!aligned(pool, 16)) return fail(KVQ_EINVAL, "copy_blocks: pool must be 16-byte aligned");
+  if (int rc = check_device()) return rc;
+  kvq::copy_blocks_kernel<<<n_pairs, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      static_cast<uint8_t*>(pool), num_blocks, Hkv, pairs);
+  return check_launch("copy_blocks");
+}
+
+}  // extern "C"

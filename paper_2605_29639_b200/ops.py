@@ -1,0 +1,145 @@
+"""Python entry points of the path (the plugin surface), each a thin call
+through the C ABI of libkvq.so.  There is no CPU fallback: a tensor that is not
+on a CUDA device, or a missing library, raises.
+
+* :func:`quantize_append`       -> ``kvq_quant_append``  (K1)
+* :func:`paged_decode_attention` -> ``kvq_decode_attn``  (K2 + fused combine)
+* :func:`copy_blocks`            -> ``kvq_copy_blocks``  (copy-on-write pages)
+"""
+from __future__ import annotations
+
+import math
+from typing import Dict, Optional, Sequence, Tuple
+
+import numpy as np
+import torch
+
+from . import _lib
+from .cache import PagedKVCache
+
+_WS_CACHE: Dict[Tuple[int, int], torch.Tensor] = {}
+
+
+def _stream_handle(device: torch.device) -> int:
+    return torch.cuda.current_stream(device).cuda_stream
+
+
+def _require_cuda(name: str, *ts: torch.Tensor) -> None:
+    for t in ts:
+        if not t.is_cuda:
+            raise ValueError(f"{name}: tensors must be on a CUDA device (no CPU fallback)")
+
+
+def quantize_append(cache: PagedKVCache, k: torch.Tensor, v: torch.Tensor,
+                    slot_mapping: torch.Tensor) -> None:
+    """Quantize new K/V rows and scatter them into their pages.
+
+    k, v: bf16 ``[T, Hkv, 128]`` (token stride may exceed ``Hkv*128``, e.g.
+    slices of a fused QKV buffer); slot_mapping: int32 ``[T]`` with
+    ``block * 16 + offset`` (negative = skip)."""
+    _require_cuda("quantize_append", k, v, slot_mapping, cache.pool)
+    spec = cache.spec
+    for name, t in (("k", k), ("v", v)):
+        if t.dtype != torch.bfloat16 or t.dim() != 3 or t.shape[1:] != (spec.num_kv_heads, 128):
+            raise ValueError(f"quantize_append: {name} must be bf16 [T, {spec.num_kv_heads}, 128]")
+        if t.stride(2) != 1 or t.stride(1) != 128:
+            raise ValueError(f"quantize_append: {name} heads must be contiguous")
+    if k.shape[0] != v.shape[0] or slot_mapping.shape != (k.shape[0],):
+        raise ValueError("quantize_append: T mismatch")
+    if slot_mapping.dtype != torch.int32 or not slot_mapping.is_contiguous():
+        raise ValueError("quantize_append: slot_mapping must be contiguous int32")
+    lib = _lib.load()
+    st = lib.kvq_quant_append(k.data_ptr(), v.data_ptr(), k.stride(0), v.stride(0),
+                              slot_mapping.data_ptr(), k.shape[0], spec.num_kv_heads,
+                              spec.kv_dtype_id, cache.pool.data_ptr(), cache.num_blocks,
+                              _stream_handle(k.device))
+    _lib.check("kvq_quant_append", st)
+
+
+def pages_per_split(batch: int, num_kv_heads: int, total_pages: int, max_blocks: int) -> int:
+    return int(_lib.load().kvq_decode_pages_per_split(batch, num_kv_heads, total_pages, max_blocks))
+
+
+def workspace_bytes(batch: int, num_q_heads: int, num_kv_heads: int, max_splits: int) -> int:
+    return int(_lib.load().kvq_decode_workspace_bytes(batch, num_q_heads, num_kv_heads, max_splits))
+
+
+def _workspace(device: torch.device, nbytes: int) -> torch.Tensor:
+    key = (device.index if device.index is not None else torch.cuda.current_device(),
+           _stream_handle(device))
+    ws = _WS_CACHE.get(key)
+    if ws is None or ws.numel() < nbytes:
+        ws = torch.zeros(max(nbytes, 1 << 20), dtype=torch.uint8, device=device)
+        _WS_CACHE[key] = ws
+    return ws
+
+
+def paged_decode_attention(q: torch.Tensor, cache: PagedKVCache, block_table: torch.Tensor,
+                           seq_lens: torch.Tensor, *, sm_scale: Optional[float] = None,
+                           pages_per_split: Optional[int] = None,
+                           total_pages: Optional[int] = None,
+                           out: Optional[torch.Tensor] = None,
+                           out_dtype: torch.dtype = torch.bfloat16, head_major: bool = False,
+                           workspace: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """GQA decode attention of one query token per sequence over the paged,
+    quantized KV cache.
+
+    q: bf16 ``[B, Hq, 128]``; block_table: int32 ``[B, max_blocks]``;
+    seq_lens: int32 ``[B]``.  Returns ``[B, Hq, 128]`` (or ``[Hq, B, 128]``
+    with ``head_major=True``, the layout the KV-head all-gather wants) in
+    ``out_dtype`` (bf16 or fp32).  ``total_pages`` (sum of per-sequence
+    pages, when the host knows it) sharpens the split-KV geometry."""
+    _require_cuda("paged_decode_attention", q, block_table, seq_lens, cache.pool)
+    spec = cache.spec
+    if q.dtype != torch.bfloat16 or q.dim() != 3 or q.shape[2] != 128 or q.stride(2) != 1:
+        raise ValueError("paged_decode_attention: q must be bf16 [B, Hq, 128]")
+    B, Hq = q.shape[0], q.shape[1]
+    if q.stride(1) != 128:
+        raise ValueError("paged_decode_attention: q heads must be contiguous")
+    if block_table.dtype != torch.int32 or block_table.dim() != 2 or block_table.shape[0] != B \
+            or not block_table.is_contiguous():
+        raise ValueError("paged_decode_attention: block_table must be contiguous int32 [B, max_blocks]")
+    if seq_lens.dtype != torch.int32 or seq_lens.shape != (B,) or not seq_lens.is_contiguous():
+        raise ValueError("paged_decode_attention: seq_lens must be contiguous int32 [B]")
+    if out_dtype not in (torch.bfloat16, torch.float32):
+        raise ValueError("paged_decode_attention: out_dtype must be bf16 or fp32")
+    max_blocks = block_table.shape[1]
+    shape = (Hq, B, 128) if head_major else (B, Hq, 128)
+    if out is None:
+        out = torch.empty(shape, dtype=out_dtype, device=q.device)
+    elif tuple(out.shape) != shape or out.dtype != out_dtype or not out.is_contiguous():
+        raise ValueError(f"paged_decode_attention: out must be contiguous {out_dtype} {shape}")
+    if B == 0:
+        return out
+    if sm_scale is None:
+        sm_scale = 1.0 / math.sqrt(128)
+    lib = _lib.load()
+    pps = pages_per_split or lib.kvq_decode_pages_per_split(
+        B, spec.num_kv_heads, total_pages if total_pages is not None else B * max_blocks, max_blocks)
+    max_splits = -(-max_blocks // pps)
+    nbytes = lib.kvq_decode_workspace_bytes(B, Hq, spec.num_kv_heads, max_splits)
+    if workspace is None:
+        workspace = _workspace(q.device, nbytes)
+    elif workspace.numel() * workspace.element_size() < nbytes:
+        raise ValueError(f"paged_decode_attention: workspace needs {nbytes} bytes")
+    st = lib.kvq_decode_attn(
+        q.data_ptr(), q.stride(0), cache.pool.data_ptr(), cache.num_blocks, block_table.data_ptr(),
+        max_blocks, seq_lens.data_ptr(), B, Hq, spec.num_kv_heads, spec.kv_dtype_id,
+        float(sm_scale), int(pps), workspace.data_ptr(),
+        workspace.numel() * workspace.element_size(), out.data_ptr(),
+        _lib.KVQ_OUT_F32 if out_dtype == torch.float32 else _lib.KVQ_OUT_BF16,
+        _lib.KVQ_OUT_HBD if head_major else _lib.KVQ_OUT_BHD, _stream_handle(q.device))
+    _lib.check("kvq_decode_attn", st)
+    return out
+
+
+def copy_blocks(cache: PagedKVCache, pairs: Sequence[Tuple[int, int]]) -> None:
+    """Apply ``(src, dst)`` whole-block page copies (fork copy-on-write)."""
+    if not pairs:
+        return
+    _require_cuda("copy_blocks", cache.pool)
+    t = torch.as_tensor(np.asarray(pairs, dtype=np.int32).reshape(-1), device=cache.device)
+    st = _lib.load().kvq_copy_blocks(cache.pool.data_ptr(), cache.num_blocks,
+                                     cache.spec.num_kv_heads, t.data_ptr(), len(pairs),
+                                     _stream_handle(cache.device))
+    _lib.check("kvq_copy_blocks", st)

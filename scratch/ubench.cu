@@ -1,0 +1,117 @@
+// Microbenchmarks for design decisions (not product code).
+#include <cstdio>
+#include <cstdint>
+#include <cuda_runtime.h>
+#include <cuda_fp16.h>
+#define CK(x) do{cudaError_t e=(x); if(e!=cudaSuccess){printf("err %s line %d\n",cudaGetErrorString(e),__LINE__);return 1;}}while(0)
+
+__global__ void hmma_f16(float* out, int iters){
+  uint32_t a0=threadIdx.x, a1=a0*3, a2=a0*5, a3=a0*7, b0=a0*11, b1=a0*13;
+  float c[8][4]={};
+  for(int i=0;i<iters;i++){
+#pragma unroll
+    for(int j=0;j<8;j++){
+      asm volatile("mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3},{%4,%5,%6,%7},{%8,%9},{%0,%1,%2,%3};"
+        :"+f"(c[j][0]),"+f"(c[j][1]),"+f"(c[j][2]),"+f"(c[j][3]):"r"(a0),"r"(a1),"r"(a2),"r"(a3),"r"(b0),"r"(b1));
+    }
+  }
+  float s=0; for(int j=0;j<8;j++) s+=c[j][0]+c[j][1]+c[j][2]+c[j][3];
+  if(s==1.2345f) out[0]=s;
+}
+__global__ void mma_e4m3(float* out, int iters){
+  uint32_t a0=threadIdx.x, a1=a0*3, a2=a0*5, a3=a0*7, b0=a0*11, b1=a0*13;
+  float c[8][4]={};
+  for(int i=0;i<iters;i++){
+#pragma unroll
+    for(int j=0;j<8;j++){
+      asm volatile("mma.sync.aligned.m16n8k32.row.col.f32.e4m3.e4m3.f32 {%0,%1,%2,%3},{%4,%5,%6,%7},{%8,%9},{%0,%1,%2,%3};"
+        :"+f"(c[j][0]),"+f"(c[j][1]),"+f"(c[j][2]),"+f"(c[j][3]):"r"(a0),"r"(a1),"r"(a2),"r"(a3),"r"(b0),"r"(b1));
+    }
+  }
+  float s=0; for(int j=0;j<8;j++) s+=c[j][0]+c[j][1]+c[j][2]+c[j][3];
+  if(s==1.2345f) out[0]=s;
+}
+__global__ void mma_s8(float* out, int iters){
+  uint32_t a0=threadIdx.x, a1=a0*3, a2=a0*5, a3=a0*7, b0=a0*11, b1=a0*13;
+  int c[8][4]={};
+  for(int i=0;i<iters;i++){
+#pragma unroll
+    for(int j=0;j<8;j++){
+      asm volatile("mma.sync.aligned.m16n8k32.row.col.s32.s8.s8.s32 {%0,%1,%2,%3},{%4,%5,%6,%7},{%8,%9},{%0,%1,%2,%3};"
+        :"+r"(c[j][0]),"+r"(c[j][1]),"+r"(c[j][2]),"+r"(c[j][3]):"r"(a0),"r"(a1),"r"(a2),"r"(a3),"r"(b0),"r"(b1));
+    }
+  }
+  int s=0; for(int j=0;j<8;j++) s+=c[j][0]+c[j][1]+c[j][2]+c[j][3];
+  if(s==12345) out[0]=s;
+}
+// conversion throughput: int8 -> f16x2 via xor/prmt/hsub2
+__global__ void cvt_i8(uint32_t* out, int iters){
+  uint32_t x = threadIdx.x*0x01030507u; uint32_t acc=0;
+  for(int i=0;i<iters;i++){
+#pragma unroll
+    for(int j=0;j<16;j++){
+      uint32_t u = x ^ 0x80808080u; uint32_t h0,h1;
+      asm volatile("prmt.b32 %0,%1,%2,0x7170;":"=r"(h0):"r"(u),"r"(0x64646464u));
+      asm volatile("prmt.b32 %0,%1,%2,0x7372;":"=r"(h1):"r"(u),"r"(0x64646464u));
+      asm volatile("sub.f16x2 %0,%0,%1;":"+r"(h0):"r"(0x64806480u));
+      asm volatile("sub.f16x2 %0,%0,%1;":"+r"(h1):"r"(0x64806480u));
+      acc ^= h0 + h1; x += acc;
+    }
+  }
+  out[blockIdx.x*blockDim.x+threadIdx.x]=acc;
+}
+__global__ void cvt_e4m3(uint32_t* out, int iters){
+  uint32_t x = threadIdx.x*0x01030507u; uint32_t acc=0;
+  for(int i=0;i<iters;i++){
+#pragma unroll
+    for(int j=0;j<16;j++){
+      uint32_t h0,h1; uint16_t lo = x & 0xffff, hi = x>>16;
+      asm volatile("cvt.rn.f16x2.e4m3x2 %0,%1;":"=r"(h0):"h"(lo));
+      asm volatile("cvt.rn.f16x2.e4m3x2 %0,%1;":"=r"(h1):"h"(hi));
+      acc ^= h0 + h1; x += acc;
+    }
+  }
+  out[blockIdx.x*blockDim.x+threadIdx.x]=acc;
+}
+__global__ void stream_ldg(const int4* __restrict__ in, size_t n, int4* out){
+  int4 acc = make_int4(0,0,0,0);
+  size_t stride = (size_t)gridDim.x*blockDim.x;
+  for(size_t i=(size_t)blockIdx.x*blockDim.x+threadIdx.x; i<n; i+=stride*4){
+    int4 v[4];
+#pragma unroll
+    for(int u=0;u<4;u++){ size_t j=i+u*stride; if(j<n){ asm volatile("ld.global.nc.L1::no_allocate.v4.s32 {%0,%1,%2,%3},[%4];":"=r"(v[u].x),"=r"(v[u].y),"=r"(v[u].z),"=r"(v[u].w):"l"(in+j));} else v[u]=make_int4(0,0,0,0);}
+#pragma unroll
+    for(int u=0;u<4;u++){acc.x^=v[u].x;acc.y^=v[u].y;acc.z^=v[u].z;acc.w^=v[u].w;}
+  }
+  if(acc.x==0x12345678) out[0]=acc;
+}
+template<class K> float timeit(K k, int grid, int block, int reps){
+  cudaEvent_t a,b; cudaEventCreate(&a); cudaEventCreate(&b);
+  k(); cudaDeviceSynchronize();
+  cudaEventRecord(a); for(int i=0;i<reps;i++) k(); cudaEventRecord(b); cudaEventSynchronize(b);
+  float ms; cudaEventElapsedTime(&ms,a,b); return ms/reps;
+}
+int main(){
+  int sms; cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  float* fo; uint32_t* uo; CK(cudaMalloc(&fo, 1<<20)); CK(cudaMalloc(&uo, 64<<20));
+  int iters=4096;
+  for(int warps: {4,8,16}){
+
+    float ms=timeit([&]{hmma_f16<<<sms, 32*warps>>>(fo,iters);}, 1,1,3);
+    double macs=(double)sms*warps*iters*8*2048; printf("hmma f16 m16n8k16 warps/SM=%d: %.1f TFLOPS (%.3f mma/clk/SM @1.9GHz)\n",warps, 2*macs/ms/1e9, macs/2048/sms/(ms*1e-3*1.9e9));
+    ms=timeit([&]{mma_e4m3<<<sms, 32*warps>>>(fo,iters);}, 1,1,3);
+    macs=(double)sms*warps*iters*8*4096; printf("mma e4m3 m16n8k32 warps/SM=%d: %.1f TFLOPS\n",warps, 2*macs/ms/1e9);
+    ms=timeit([&]{mma_s8<<<sms, 32*warps>>>(fo,iters);}, 1,1,3);
+    printf("mma s8 m16n8k32 warps/SM=%d: %.1f TOPS\n",warps, 2*macs/ms/1e9);
+    ms=timeit([&]{cvt_i8<<<sms, 32*warps>>>(uo,iters);}, 1,1,3);
+    double bytes=(double)sms*warps*32*iters*16*4; printf("cvt i8->f16 warps/SM=%d: %.1f Gbyte/s converted (%.1f B/clk/SM)\n",warps, bytes/ms/1e6, bytes/sms/(ms*1e-3*1.9e9));
+    ms=timeit([&]{cvt_e4m3<<<sms, 32*warps>>>(uo,iters);}, 1,1,3);
+    printf("cvt e4m3->f16 warps/SM=%d: %.1f Gbyte/s converted (%.1f B/clk/SM)\n",warps, bytes/ms/1e6, bytes/sms/(ms*1e-3*1.9e9));
+  }
+  size_t nbytes = 4ull<<30; int4* in; CK(cudaMalloc(&in, nbytes)); cudaMemset(in, 1, nbytes);
+  for(int bpsm: {2,4,8}) for(int thr: {256,512}){
+    float ms=timeit([&]{stream_ldg<<<sms*bpsm, thr>>>(in, nbytes/16, (int4*)fo);},1,1,5);
+    printf("stream LDG.128 grid=%d*%d thr=%d: %.1f GB/s\n", sms, bpsm, thr, nbytes/ms/1e6);
+  }
+  return 0;
+}

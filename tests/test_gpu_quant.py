@@ -1,0 +1,84 @@
+"""K1 (quantize-on-append) parity on the B200: pool bytes bit-exact with the
+CPU oracle (codes AND fp32 scales, same rounding mode), including the
+contract's edge cases."""
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+from kvq_testutil import bf16_bits, make_kv
+from paper_2605_29639_b200 import KVCacheSpec, PagedKVCache, quantize_append, unpack_pages
+
+pytestmark = pytest.mark.gpu
+DT = {"int8": O.INT8, "fp8_e4m3": O.FP8_E4M3}
+
+
+def run_both(k, v, slots, Hkv, kv_dtype, num_blocks, cuda):
+    cache = PagedKVCache(KVCacheSpec(Hkv, kv_dtype=kv_dtype), num_blocks, device=cuda)
+    quantize_append(cache, k.to(cuda), v.to(cuda), torch.as_tensor(slots, dtype=torch.int32, device=cuda))
+    gpu = cache.pool.cpu().numpy()
+    ref = np.zeros((num_blocks, Hkv, O.PAGE), dtype=np.uint8)
+    O.quant_append(bf16_bits(k), bf16_bits(v), slots, DT[kv_dtype], ref)
+    return gpu, ref
+
+
+@pytest.mark.parametrize("kv_dtype", ["int8", "fp8_e4m3"])
+@pytest.mark.parametrize("T,Hkv", [(1, 8), (37, 4), (256, 8), (2048, 8), (300, 1)])
+def test_append_bit_exact(cuda, kv_dtype, T, Hkv):
+    num_blocks = (T + 15) // 16 + 5
+    rng = np.random.default_rng(T * 7 + Hkv)
+    slots = rng.permutation(num_blocks * 16)[:T].astype(np.int32)
+    k, v = make_kv(T, Hkv, 1, kind="k"), make_kv(T, Hkv, 2, kind="v")
+    gpu, ref = run_both(k, v, slots, Hkv, kv_dtype, num_blocks, cuda)
+    assert np.array_equal(gpu, ref), f"{(gpu != ref).sum()} bytes differ"
+    codes, scales = unpack_pages(torch.from_numpy(gpu))
+    c2, s2 = O.unpack_pool(ref)
+    assert np.array_equal(codes.numpy(), c2)
+    assert np.array_equal(scales.numpy().view(np.uint32), s2.view(np.uint32))
+
+
+def edge_rows():
+    rows = []
+    r = np.zeros(128, np.float32); rows.append(r)                      # all zero -> scale 0, codes 0
+    r = np.zeros(128, np.float32); r[5] = -0.0; r[6] = 1e-3; rows.append(r)
+    r = np.linspace(-127.5, 127.5, 128).astype(np.float32); rows.append(r)
+    r = np.full(128, 0.5, np.float32); r[0] = 127.0; r[1:6] = [0.5, 1.5, 2.5, -0.5, -2.5]; rows.append(r)
+    r = np.full(128, 448.0, np.float32); r[1:8] = [1.0625, 1.1875, 464, 479.99, -500, 2**-10, 3 * 2**-11]; rows.append(r)
+    r = np.full(128, 1e-39, np.float32); r[3] = 9.2e-41; rows.append(r)   # bf16 subnormals
+    r = np.ones(128, np.float32); r[7] = np.nan; rows.append(r)
+    r = np.ones(128, np.float32); r[9] = np.inf; rows.append(r)
+    r = np.ones(128, np.float32); r[9] = -np.inf; r[10] = np.nan; rows.append(r)
+    r = np.full(128, 3e38, np.float32); r[2] = -3.3e38; rows.append(r)
+    rng = np.random.default_rng(5)
+    for e in (-30, -8, 0, 8, 30):
+        rows.append((rng.standard_normal(128) * 2.0 ** e).astype(np.float32))
+    return np.stack(rows)
+
+
+@pytest.mark.parametrize("kv_dtype", ["int8", "fp8_e4m3"])
+def test_append_edge_cases(cuda, kv_dtype):
+    x = edge_rows()
+    T = x.shape[0]
+    bits = O.f32_to_bf16_bits(x)
+    k = torch.from_numpy(bits.view(np.int16)).view(torch.bfloat16).reshape(T, 1, 128)
+    v = torch.from_numpy(bits[::-1].copy().view(np.int16)).view(torch.bfloat16).reshape(T, 1, 128)
+    slots = np.arange(T, dtype=np.int32)
+    gpu, ref = run_both(k, v, slots, 1, kv_dtype, (T + 15) // 16, cuda)
+    diff = np.nonzero(gpu != ref)
+    assert diff[0].size == 0, f"mismatch at {list(zip(*diff))[:8]}: gpu {gpu[diff][:8]} ref {ref[diff][:8]}"
+
+
+def test_append_strided_and_skipped(cuda):
+    T, Hkv = 64, 8
+    qkv = make_kv(T, 3 * Hkv, 9).reshape(T, 3 * Hkv, 128)   # fused [T, (Hq+2Hkv), d] style buffer
+    k, v = qkv[:, Hkv:2 * Hkv], qkv[:, 2 * Hkv:]
+    slots = np.arange(T, dtype=np.int32) + 16
+    slots[::5] = -1
+    cache = PagedKVCache(KVCacheSpec(Hkv), 6, device=cuda)
+    qkv_d = qkv.to(cuda)
+    quantize_append(cache, qkv_d[:, Hkv:2 * Hkv], qkv_d[:, 2 * Hkv:],
+                    torch.as_tensor(slots, device=cuda))
+    ref = np.zeros((6, Hkv, O.PAGE), dtype=np.uint8)
+    O.quant_append(bf16_bits(k.contiguous()), bf16_bits(v.contiguous()), slots, O.INT8, ref)
+    assert np.array_equal(cache.pool.cpu().numpy(), ref)
+    assert not ref[0].any(), "block 0 must stay untouched"

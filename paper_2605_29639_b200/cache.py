@@ -24,6 +24,7 @@ decoupled from the reference's prefix-hash granularity (64 tokens,
 """
 from __future__ import annotations
 
+import heapq
 from dataclasses import dataclass, field
 from typing import Dict, Iterable, List, Optional, Sequence, Tuple
 
@@ -144,59 +145,204 @@ def unpack_pages(pages: torch.Tensor) -> Tuple[torch.Tensor, torch.Tensor]:
 
 
 # ---------------------------------------------------------------------------
-# Block allocator (host bookkeeping; device pages are copied by kvq_copy_blocks)
+# Block pool: residency + lifecycle of physical pages (the reference's GPU tier)
 # ---------------------------------------------------------------------------
 @dataclass
-class _Block:
+class BlockEntry:
+    """One resident page set (the reference's ``CacheBlockEntry``,
+    ``tiered_cache.py:105-116``) plus the physical block it occupies."""
+
+    key: object
+    block: int
+    seq_no: int          # insertion order: the reference's monotonic block_id (LRU tie-break)
+    watermark: int
     ref_count: int = 0
-    watermark: int = 0
+    last_access: int = 0
 
 
+class BlockPool:
+    """Residency of ``num_blocks`` physical pages under the reference GPU-tier
+    rules: insert (evicting least-recently-used unreferenced entries, ties by
+    insertion order, ``tiered_cache.py:189-252``), acquire (partial blocks are
+    exclusive, ``:355-363``), release (``:327-342``), grow-only watermark
+    (``:344-351``).  Unreferenced entries stay resident (reusable by key) until
+    evicted or dropped."""
+
+    def __init__(self, num_blocks: int, block_size: int = BLOCK_SIZE, bytes_per_block: int = 1):
+        if num_blocks <= 0:
+            raise ValueError("num_blocks must be positive")
+        self.num_blocks, self.block_size, self.bytes_per_block = num_blocks, block_size, bytes_per_block
+        self._free: List[int] = list(range(num_blocks - 1, -1, -1))  # pop() -> lowest id first
+        self._entries: Dict[object, BlockEntry] = {}
+        self._heap: List[Tuple[int, int, object]] = []  # lazy (last_access, seq_no, key)
+        self._by_block: Dict[int, object] = {}
+        self._seq = 0
+        self.mutation_count = 0
+
+    # -- introspection
+    def __len__(self) -> int:
+        return len(self._entries)
+
+    @property
+    def num_free(self) -> int:
+        return len(self._free)
+
+    def entry(self, key) -> Optional[BlockEntry]:
+        return self._entries.get(key)
+
+    def key_of(self, block: int):
+        return self._by_block.get(block)
+
+    def lookup(self, key) -> Optional[int]:
+        e = self._entries.get(key)
+        return None if e is None else e.block
+
+    def keys(self):
+        return list(self._entries)
+
+    def is_partial(self, e: BlockEntry) -> bool:
+        return e.watermark < self.block_size
+
+    # -- mutation
+    def insert(self, key, watermark: int, clock: int = 0) -> int:
+        if not 0 <= watermark <= self.block_size:
+            raise ValueError("watermark out of range")
+        if key in self._entries:
+            raise ValueError("duplicate insert")
+        if not self._free:
+            self.evict(1)
+        blk = self._free.pop()
+        e = BlockEntry(key=key, block=blk, seq_no=self._seq, watermark=watermark, last_access=clock)
+        self._seq += 1
+        self._entries[key] = e
+        self._by_block[blk] = key
+        self.mutation_count += 1
+        heapq.heappush(self._heap, (clock, e.seq_no, key))
+        return blk
+
+    def evict(self, nblocks: int) -> List[object]:
+        """Drop unreferenced entries, oldest first; partial progress stands
+        when it raises (as the reference's ``evict``)."""
+        if nblocks <= 0:
+            raise ValueError("bytes_needed must be positive")
+        out: List[object] = []
+        while len(out) < nblocks:
+            while self._heap:
+                la, sq, k = self._heap[0]
+                e = self._entries.get(k)
+                if e is not None and e.ref_count == 0 and e.last_access == la and e.seq_no == sq:
+                    break
+                heapq.heappop(self._heap)
+            if not self._heap:
+                raise CacheThrashError((nblocks - len(out)) * self.bytes_per_block)
+            _, _, k = heapq.heappop(self._heap)
+            self.drop(k)
+            out.append(k)
+        return out
+
+    def drop(self, key) -> int:
+        e = self._entries.pop(key)
+        if e.ref_count:
+            self._entries[key] = e
+            raise ValueError("cannot drop a referenced block")
+        self._free.append(e.block)
+        del self._by_block[e.block]
+        self.mutation_count += 1
+        return e.block
+
+    def acquire(self, key, clock: int = 0) -> BlockEntry:
+        e = self._entries.get(key)
+        if e is None:
+            raise KeyError(f"no entry for {key!r}")
+        if self.is_partial(e) and e.ref_count >= 1:
+            raise ValueError("partial block is exclusive")
+        e.ref_count += 1
+        self._touch(e, clock)
+        return e
+
+    def release(self, keys: Iterable, clock: int = 0) -> None:
+        for k in keys:
+            e = self._entries.get(k)
+            if e is None or e.ref_count <= 0:
+                raise ValueError("double release")
+            e.ref_count -= 1
+            self._touch(e, clock)
+
+    def set_watermark(self, key, watermark: int) -> None:
+        e = self._entries.get(key)
+        if e is None:
+            raise KeyError(f"no entry for {key!r}")
+        if not e.watermark <= watermark <= self.block_size:
+            raise ValueError("watermark may only grow, up to block_size")
+        e.watermark = watermark
+
+    def rekey(self, old, new) -> None:
+        """Give a resident entry a new key (e.g. its content hash once full)."""
+        if new in self._entries:
+            raise ValueError("duplicate insert")
+        e = self._entries.pop(old)
+        e.key = new
+        self._entries[new] = e
+        self._by_block[e.block] = new
+        if e.ref_count == 0:
+            heapq.heappush(self._heap, (e.last_access, e.seq_no, new))
+
+    def _touch(self, e: BlockEntry, clock: int) -> None:
+        e.last_access = clock
+        if e.ref_count == 0:
+            heapq.heappush(self._heap, (clock, e.seq_no, e.key))
+
+
+# ---------------------------------------------------------------------------
+# Block allocator (sequences on top of the pool; device pages are copied by
+# kvq_copy_blocks)
+# ---------------------------------------------------------------------------
 @dataclass
 class _Seq:
-    blocks: List[int] = field(default_factory=list)
+    keys: List[object] = field(default_factory=list)
     length: int = 0
 
 
 class BlockAllocator:
-    """Free list + refcounts + per-sequence block lists.
+    """Per-sequence block lists over a :class:`BlockPool`.
 
     ``append_slots`` returns the slot ids (``block * 16 + offset``) the new
     tokens occupy; ``fork`` shares every full block of the parent and copies
     its partial tail (partial blocks are exclusive), returning the
     ``(src, dst)`` page copies the caller must apply on the device before the
-    child appends.
+    child appends.  Private blocks are returned to the free list as soon as
+    their last reference is released.
     """
 
     def __init__(self, num_blocks: int, block_size: int = BLOCK_SIZE, bytes_per_block: int = 1):
-        if num_blocks <= 0:
-            raise ValueError("num_blocks must be positive")
         if block_size != BLOCK_SIZE:
             raise ValueError(f"block_size must be {BLOCK_SIZE}")
-        self.num_blocks = num_blocks
-        self.block_size = block_size
+        self.pool = BlockPool(num_blocks, block_size, bytes_per_block)
+        self.num_blocks, self.block_size = num_blocks, block_size
         self.bytes_per_block = bytes_per_block
-        self._blocks = [_Block() for _ in range(num_blocks)]
-        # LIFO free list, lowest ids handed out first (deterministic replay).
-        self._free: List[int] = list(range(num_blocks - 1, -1, -1))
         self._seqs: Dict[object, _Seq] = {}
+        self._anon = 0
+        self.clock = 0
 
-    # -- introspection ------------------------------------------------------
+    # -- introspection
     @property
     def num_free(self) -> int:
-        return len(self._free)
+        return self.pool.num_free
+
+    def _entry_of_block(self, block: int) -> Optional[BlockEntry]:
+        k = self.pool.key_of(block)
+        return None if k is None else self.pool.entry(k)
 
     def ref_count(self, block: int) -> int:
-        return self._blocks[block].ref_count
+        e = self._entry_of_block(block)
+        return 0 if e is None else e.ref_count
 
     def watermark(self, block: int) -> int:
-        return self._blocks[block].watermark
-
-    def is_full(self, block: int) -> bool:
-        return self._blocks[block].watermark == self.block_size
+        e = self._entry_of_block(block)
+        return 0 if e is None else e.watermark
 
     def block_ids(self, seq_id) -> List[int]:
-        return list(self._seq(seq_id).blocks)
+        return [self.pool.lookup(k) for k in self._seq(seq_id).keys]
 
     def seq_len(self, seq_id) -> int:
         return self._seq(seq_id).length
@@ -213,37 +359,21 @@ class BlockAllocator:
         except KeyError:
             raise KeyError(f"unknown sequence {seq_id!r}") from None
 
-    # -- block primitives (the reference's acquire / release / set_watermark)
-    def _new_block(self) -> int:
-        if not self._free:
+    def _new_block(self) -> object:
+        key = ("anon", self._anon)
+        self._anon += 1
+        if not self.pool.num_free:
             raise CacheThrashError(self.bytes_per_block)
-        blk = self._free.pop()
-        self._blocks[blk] = _Block(ref_count=0, watermark=0)
-        self._acquire(blk)
-        return blk
+        self.pool.insert(key, 0, self.clock)
+        self.pool.acquire(key, self.clock)
+        return key
 
-    def _acquire(self, blk: int) -> None:
-        e = self._blocks[blk]
-        if e.watermark < self.block_size and e.ref_count >= 1:
-            raise ValueError("partial block is exclusive")
-        e.ref_count += 1
+    def _release(self, key) -> None:
+        self.pool.release([key], self.clock)
+        if self.pool.entry(key).ref_count == 0:
+            self.pool.drop(key)
 
-    def _release(self, blk: int) -> None:
-        e = self._blocks[blk]
-        if e.ref_count <= 0:
-            raise ValueError("double release")
-        e.ref_count -= 1
-        if e.ref_count == 0:
-            e.watermark = 0
-            self._free.append(blk)
-
-    def _set_watermark(self, blk: int, watermark: int) -> None:
-        e = self._blocks[blk]
-        if not e.watermark <= watermark <= self.block_size:
-            raise ValueError("watermark may only grow, up to block_size")
-        e.watermark = watermark
-
-    # -- sequence API ---------------------------------------------------------
+    # -- sequence API
     def allocate(self, seq_id) -> None:
         """Register an empty sequence."""
         if seq_id in self._seqs:
@@ -251,28 +381,29 @@ class BlockAllocator:
         self._seqs[seq_id] = _Seq()
 
     def append_slots(self, seq_id, n: int) -> List[int]:
-        """Reserve ``n`` token slots at the end of ``seq_id``.
-
-        Atomic: on :class:`CacheThrashError` nothing changes."""
+        """Reserve ``n`` token slots at the end of ``seq_id``.  Atomic: on
+        :class:`CacheThrashError` nothing changes."""
         if n < 0:
             raise ValueError("n must be >= 0")
         s = self._seq(seq_id)
         bs = self.block_size
-        tail_room = (bs - s.length % bs) % bs if s.blocks else 0
+        tail_room = (bs - s.length % bs) % bs if s.keys else 0
         new_blocks = -(-(n - tail_room) // bs) if n > tail_room else 0
-        if new_blocks > len(self._free):
-            raise CacheThrashError((new_blocks - len(self._free)) * self.bytes_per_block)
+        if new_blocks > self.pool.num_free:
+            raise CacheThrashError((new_blocks - self.pool.num_free) * self.bytes_per_block)
+        self.clock += 1
         slots: List[int] = []
         pos = s.length
-        for _ in range(n):
-            if pos % bs == 0 and pos // bs == len(s.blocks):
-                s.blocks.append(self._new_block())
-            blk = s.blocks[pos // bs]
-            # Appends only ever land in an exclusively-owned (partial) block.
-            assert self._blocks[blk].ref_count == 1
-            slots.append(blk * bs + pos % bs)
-            pos += 1
-            self._set_watermark(blk, pos - (pos - 1) // bs * bs)
+        while len(slots) < n:
+            if pos % bs == 0:
+                s.keys.append(self._new_block())
+            key = s.keys[pos // bs]
+            e = self.pool.entry(key)
+            take = min(n - len(slots), bs - pos % bs)
+            base = e.block * bs + pos % bs
+            slots.extend(range(base, base + take))
+            pos += take
+            self.pool.set_watermark(key, pos - (pos - 1) // bs * bs)
         s.length = pos
         return slots
 
@@ -282,33 +413,35 @@ class BlockAllocator:
         if child_id in self._seqs:
             raise ValueError(f"sequence {child_id!r} already exists")
         p = self._seq(parent_id)
-        copies: List[Tuple[int, int]] = []
-        blocks: List[int] = []
-        partial_tail = p.blocks and not self.is_full(p.blocks[-1])
-        if partial_tail and not self._free:
+        self.clock += 1
+        tail = p.keys[-1] if p.keys else None
+        partial_tail = tail is not None and self.pool.is_partial(self.pool.entry(tail))
+        if partial_tail and not self.pool.num_free:
             raise CacheThrashError(self.bytes_per_block)
-        for blk in p.blocks[:-1] if partial_tail else p.blocks:
-            self._acquire(blk)  # full: shareable
-            blocks.append(blk)
+        keys: List[object] = []
+        for k in (p.keys[:-1] if partial_tail else p.keys):
+            self.pool.acquire(k, self.clock)  # full: shareable
+            keys.append(k)
+        copies: List[Tuple[int, int]] = []
         if partial_tail:
-            src = p.blocks[-1]
             dst = self._new_block()
-            self._set_watermark(dst, self.watermark(src))
-            blocks.append(dst)
-            copies.append((src, dst))
-        self._seqs[child_id] = _Seq(blocks=blocks, length=p.length)
+            self.pool.set_watermark(dst, self.pool.entry(tail).watermark)
+            keys.append(dst)
+            copies.append((self.pool.lookup(tail), self.pool.lookup(dst)))
+        self._seqs[child_id] = _Seq(keys=keys, length=p.length)
         return copies
 
     def free(self, seq_id) -> None:
         s = self._seqs.pop(seq_id, None)
         if s is None:
             raise KeyError(f"unknown sequence {seq_id!r}")
-        for blk in s.blocks:
-            self._release(blk)
+        self.clock += 1
+        for k in s.keys:
+            self._release(k)
 
-    # -- device views ---------------------------------------------------------
+    # -- device views
     def block_table(self, seq_ids: Sequence, max_blocks: Optional[int] = None) -> np.ndarray:
-        rows = [self._seq(s).blocks for s in seq_ids]
+        rows = [self.block_ids(s) for s in seq_ids]
         mb = max_blocks if max_blocks is not None else max([len(r) for r in rows] + [1])
         out = np.zeros((len(rows), mb), dtype=np.int32)
         for i, r in enumerate(rows):
@@ -320,23 +453,27 @@ class BlockAllocator:
     def seq_lens(self, seq_ids: Sequence) -> np.ndarray:
         return np.array([self._seq(s).length for s in seq_ids], dtype=np.int32)
 
-    # -- invariants (for tests; cf. test_tiered_cache.py:243-327) ---------------
+    # -- invariants (for tests; cf. test_tiered_cache.py:243-327)
     def check_invariants(self) -> None:
-        counts = [0] * self.num_blocks
+        counts: Dict[object, int] = {}
         for s in self._seqs.values():
-            assert len(s.blocks) == -(-s.length // self.block_size), "block count vs length"
-            for i, blk in enumerate(s.blocks):
-                counts[blk] += 1
+            assert len(s.keys) == -(-s.length // self.block_size), "block count vs length"
+            for i, k in enumerate(s.keys):
+                counts[k] = counts.get(k, 0) + 1
                 full = (i + 1) * self.block_size <= s.length
                 wm = self.block_size if full else s.length - i * self.block_size
-                assert self._blocks[blk].watermark == wm, "watermark mismatch"
-        free = set(self._free)
-        assert len(free) == len(self._free), "free list duplicates"
-        for blk, e in enumerate(self._blocks):
-            assert e.ref_count == counts[blk], f"refcount mismatch on block {blk}"
-            assert (e.ref_count == 0) == (blk in free), "free list vs refcount"
+                assert self.pool.entry(k).watermark == wm, "watermark mismatch"
+        blocks = set()
+        for k, e in self.pool._entries.items():
+            assert e.ref_count == counts.get(k, 0), f"refcount mismatch on {k!r}"
+            assert e.block not in blocks, "physical block mapped twice"
+            blocks.add(e.block)
             if e.watermark < self.block_size:
                 assert e.ref_count <= 1, "shared partial block"
+        free = set(self.pool._free)
+        assert len(free) == len(self.pool._free), "free list duplicates"
+        assert not (free & blocks), "free block still mapped"
+        assert len(free) + len(blocks) == self.num_blocks, "blocks lost"
 
 
 class BlockTable:

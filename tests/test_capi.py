@@ -1,0 +1,72 @@
+"""The C-ABI library (libkvq.so) loads and exports exactly what include/kvq.h
+declares; host-only entry points and argument validation work without a GPU."""
+import ctypes
+import re
+from pathlib import Path
+
+import pytest
+
+from paper_2605_29639_b200 import _lib
+
+HEADER = Path(__file__).resolve().parents[1] / "include" / "kvq.h"
+
+
+def declared_functions():
+    src = re.sub(r"/\*.*?\*/", "", HEADER.read_text(), flags=re.S)
+    return re.findall(r"^\s*(?:const\s+)?[a-z_0-9]+\s*\*?\s*(kvq_[a-z_0-9]+)\s*\(", src, flags=re.M)
+
+
+def test_header_matches_binding():
+    names = declared_functions()
+    assert len(names) == 8
+    assert set(names) == set(_lib.SIGNATURES)
+
+
+def test_library_exports_every_symbol():
+    lib = ctypes.CDLL(str(_lib.LIB_PATH))
+    for name in declared_functions():
+        assert hasattr(lib, name), name
+    L = _lib.load()
+    assert L.kvq_version() == 1 and L.kvq_page_bytes() == 4224
+
+
+def test_host_only_entry_points():
+    L = _lib.load()
+    # split geometry: <= 64 pages, >= 8 pages, <= max_blocks
+    assert L.kvq_decode_pages_per_split(256, 8, 70400, 513) == 64
+    assert 8 <= L.kvq_decode_pages_per_split(8, 8, 8 * 129, 129) <= 64
+    assert L.kvq_decode_pages_per_split(1, 1, 3, 3) == 3
+    ws = L.kvq_decode_workspace_bytes(4, 32, 8, 3)
+    assert ws >= 4 * 32 * 3 * 129 * 4 + 4 * 8 * 4
+
+
+def test_argument_validation_without_gpu():
+    L = _lib.load()
+    st = L.kvq_quant_append(None, None, 128, 128, None, 4, 0, 0, None, 1, None)
+    assert st == _lib.KVQ_EINVAL and b"bad sizes" in L.kvq_last_error()
+    st = L.kvq_quant_append(16, 16, 1024, 1024, 16, 4, 8, 7, 16, 1, None)
+    assert st == _lib.KVQ_EUNSUPPORTED
+    st = L.kvq_decode_attn(16, 4096, 16, 10, 16, 4, 16, 2, 20, 8, 0, 0.1, 0, 256, 1 << 20, 16, 0, 0, None)
+    assert st == _lib.KVQ_EINVAL and b"Hq % Hkv" in L.kvq_last_error()
+    assert L.kvq_copy_blocks(None, 1, 1, None, 0, None) == 0   # no-op
+    with pytest.raises(ValueError):
+        _lib.check("kvq_decode_attn", _lib.KVQ_EINVAL)
+
+
+def test_ops_refuse_cpu_tensors():
+    import torch
+    from paper_2605_29639_b200 import KVCacheSpec, PagedKVCache, quantize_append
+    cache = PagedKVCache(KVCacheSpec(2), 4, device="cpu")
+    k = torch.zeros((3, 2, 128), dtype=torch.bfloat16)
+    with pytest.raises(ValueError, match="no CPU fallback"):
+        quantize_append(cache, k, k, torch.zeros(3, dtype=torch.int32))
+
+
+def test_no_device_is_a_loud_error():
+    """Without a GPU the product path fails (ECUDA), it never computes on CPU."""
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    L = _lib.load()
+    st = L.kvq_decode_attn(16, 4096, 16, 10, 16, 4, 16, 2, 32, 8, 0, 0.1, 0, 256, 1 << 20, 16, 0, 0, None)
+    assert st == _lib.KVQ_ECUDA

@@ -154,6 +154,11 @@ __device__ __forceinline__ uint4 lds128(const uint8_t* p) {
                : "r"(smem_u32(p)));
   return r;
 }
+__device__ __forceinline__ float lds32f(const uint8_t* p) {
+  float r;
+  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(r) : "r"(smem_u32(p)));
+  return r;
+}
 __device__ __forceinline__ float2 lds64f(const uint8_t* p) {
   float2 r;
   asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(r.x), "=f"(r.y) : "r"(smem_u32(p)));
@@ -223,13 +228,20 @@ struct DecodeParams {
   int out_f32, out_hbd;
 };
 
-constexpr int NW = 4;      // warps per CTA; every warp streams its own pages
-constexpr int S = 4;       // ring slots per warp (pages in flight per warp)
+constexpr int NW = 4;  // warps per CTA; every warp streams its own pages
 constexpr int THREADS = 32 * NW;
-constexpr int CTAS_PER_SM = 3;
-constexpr size_t DECODE_SMEM = (size_t)NW * S * PAGE + NW * S * sizeof(uint64_t) + 16;
-static_assert((size_t)NW * S * PAGE >= (size_t)NW * 16 * HD * 4 + 2 * NW * 16 * 4,
-              "merge scratch must fit in the ring");
+
+// Per-variant geometry.  NT = n-tiles of 8 query heads (g <= 8 -> 1, g <= 16 -> 2).
+template <bool HI>
+struct Geo {
+  static constexpr int NT = HI ? 2 : 1;
+  static constexpr int S = HI ? 4 : 3;            // ring slots (pages in flight) per warp
+  static constexpr int CTAS = HI ? 3 : 4;         // resident CTAs per SM (regs + smem)
+  static constexpr size_t SMEM = (size_t)NW * S * PAGE + NW * S * sizeof(uint64_t) + 16;
+  static_assert((size_t)NW * S * PAGE >= (size_t)NW * 16 * HD * 4 + 2 * NW * 16 * 4,
+                "merge scratch must fit in the ring");
+};
+constexpr int CTAS_PER_SM = 4;  // used by the split heuristic (g <= 8 variant)
 
 __device__ __forceinline__ void store_out(const DecodeParams& p, int b, int head, int d0,
                                           const float* vals) {
@@ -254,8 +266,15 @@ __device__ __forceinline__ void store_out(const DecodeParams& p, int b, int head
   }
 }
 
+__device__ __forceinline__ uint32_t movmatrix_trans(uint32_t x) {
+  uint32_t y;
+  asm("movmatrix.sync.aligned.m8n8.trans.b16 %0, %1;" : "=r"(y) : "r"(x));
+  return y;
+}
+
 // Per-warp page stream: warp w of the CTA owns pages w, w + NW, w + 2NW, ...
 // of the split; page j of the warp lands in slot j % S of the warp's ring.
+template <int S>
 struct PageStream {
   const int32_t* bt;       // block table row, offset to the split's first page
   const uint8_t* head_base;
@@ -277,7 +296,7 @@ struct PageStream {
   __device__ __forceinline__ void init(int lane) {
     base = 0;
     cur = load_ids(0, lane);
-    nxt = load_ids(32, lane);
+    nxt = nj > 32 ? load_ids(32, lane) : 0;
   }
   // Issue the bulk copy of page j (j >= base, all lanes participate).
   __device__ __forceinline__ void issue(int j, int lane) {
@@ -295,8 +314,21 @@ struct PageStream {
   }
 };
 
+// Thread mapping (lane = 4r + c).  Tensor-core tiles put the 16 tokens of a
+// page (QK^T) and 16-row slices of d (PV) on M, the query heads of the GQA
+// group on N (8 per n-tile):
+//   QK^T : S^T[16 tok x 8 heads]  = K[16 x 128]  . Q^T     (8 k-steps)
+//   PV   : O^T[16 d x 8 heads]   += V^T[16 x 16 tok] . P'^T (8 m-tiles)
+// K rows are token rows of the page; V is stored token-pair interleaved so a
+// 32-bit word holds (d, t0), (d, t1), (d+1, t0), (d+1, t1) -- exactly two
+// f16x2 A-fragment registers.  P'^T comes from the S^T accumulator through one
+// movmatrix transpose per 8x8 block.  d is permuted inside each k-step /
+// m-tile so every thread reads 16-byte chunks (bank-conflict-free given the
+// page swizzle).
 template <int KVD, bool HI>
-__global__ void __launch_bounds__(THREADS, CTAS_PER_SM) decode_kernel(const DecodeParams p) {
+__global__ void __launch_bounds__(THREADS, Geo<HI>::CTAS) decode_kernel(const DecodeParams p) {
+  constexpr int NT = Geo<HI>::NT;
+  constexpr int S = Geo<HI>::S;
   extern __shared__ __align__(128) uint8_t smem[];
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + NW * S * PAGE);
   int* flag = reinterpret_cast<int*>(bars + NW * S);
@@ -318,7 +350,7 @@ __global__ void __launch_bounds__(THREADS, CTAS_PER_SM) decode_kernel(const Deco
   const int pg0 = split * p.pages_per_split;
   const int n = min(npages, pg0 + p.pages_per_split) - pg0;
 
-  PageStream ps;
+  PageStream<S> ps;
   ps.bt = p.block_table + (int64_t)b * p.max_blocks + pg0;
   ps.head_base = p.pool + (int64_t)h * PAGE;
   ps.blk_stride = (int64_t)p.Hkv * PAGE;
@@ -338,34 +370,32 @@ __global__ void __launch_bounds__(THREADS, CTAS_PER_SM) decode_kernel(const Deco
 #pragma unroll 1
   for (int j = 0; j < S && j < ps.nj; ++j) ps.issue(j, lane);
 
-  const int r = lane >> 2, cc = lane & 3;
-  const bool row_lo_valid = r < g;
-  const bool row_hi_valid = HI && (r + 8 < g);
+  const int r = lane >> 2, c = lane & 3;
 
-  // Q fragments: head row r (and r + 8), d ranges [16cc, 16cc+16) and [64+16cc, +16).
-  // k-step i covers d = base(i) + {0,1} (a0/a1) and base(i) + {2,3} (a2/a3),
-  // base(i) = (i < 4 ? 16cc + 4i : 64 + 16cc + 4(i-4)).
-  uint32_t qlo[8][2], qhi[8][2];
+  // Q^T B-fragments: n-tile nt holds head 8nt + r; k-step i covers
+  // d = base(i) + {0,1} (b0) and base(i) + {2,3} (b1),
+  // base(i) = (i < 4 ? 16c + 4i : 64 + 16c + 4(i-4)).
+  uint32_t qf[NT][8][2];
   float qscale;
   {
     const __nv_bfloat16* qrow = p.q + (int64_t)b * p.q_stride_b + (int64_t)(h * g) * HD;
-    uint4 raw[2][4];
+    uint4 raw[NT][4];
 #pragma unroll
-    for (int rr = 0; rr < 2; ++rr) {
-      const bool valid = rr == 0 ? row_lo_valid : row_hi_valid;
-      const __nv_bfloat16* src = qrow + (r + 8 * rr) * HD;
+    for (int nt = 0; nt < NT; ++nt) {
+      const bool valid = 8 * nt + r < g;
+      const __nv_bfloat16* src = qrow + (8 * nt + r) * HD;
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
-        const int d = (u < 2 ? 16 * cc + 8 * u : 64 + 16 * cc + 8 * (u - 2));
-        raw[rr][u] = valid ? __ldg(reinterpret_cast<const uint4*>(src + d)) : make_uint4(0, 0, 0, 0);
+        const int d = (u < 2 ? 16 * c + 8 * u : 64 + 16 * c + 8 * (u - 2));
+        raw[nt][u] = valid ? __ldg(reinterpret_cast<const uint4*>(src + d)) : make_uint4(0, 0, 0, 0);
       }
     }
     float amax = 0.0f;
 #pragma unroll
-    for (int rr = 0; rr < 2; ++rr)
+    for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
-        const uint32_t w[4] = {raw[rr][u].x, raw[rr][u].y, raw[rr][u].z, raw[rr][u].w};
+        const uint32_t w[4] = {raw[nt][u].x, raw[nt][u].y, raw[nt][u].z, raw[nt][u].w};
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
           amax = fmaxf(amax, fabsf(__uint_as_float(w[e] << 16)));
@@ -380,39 +410,52 @@ __global__ void __launch_bounds__(THREADS, CTAS_PER_SM) decode_kernel(const Deco
     const float pre = pow2i(14 - ex);
     qscale = p.sm_scale_log2 / pre;
 #pragma unroll
-    for (int rr = 0; rr < 2; ++rr)
+    for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
-        const uint32_t w[4] = {raw[rr][u].x, raw[rr][u].y, raw[rr][u].z, raw[rr][u].w};
+        const uint32_t w[4] = {raw[nt][u].x, raw[nt][u].y, raw[nt][u].z, raw[nt][u].w};
         uint32_t hw[4];
 #pragma unroll
         for (int e = 0; e < 4; ++e)
           hw[e] = pack_half2(__uint_as_float(w[e] << 16) * pre,
                              __uint_as_float(w[e] & 0xffff0000u) * pre);
         const int i0 = 2 * u;  // uint4 u holds d = base(i0) .. base(i0) + 7
-        uint32_t(&dst)[8][2] = rr == 0 ? qlo : qhi;
-        dst[i0][0] = hw[0];
-        dst[i0][1] = hw[1];
-        dst[i0 + 1][0] = hw[2];
-        dst[i0 + 1][1] = hw[3];
+        qf[nt][i0][0] = hw[0];
+        qf[nt][i0][1] = hw[1];
+        qf[nt][i0 + 1][0] = hw[2];
+        qf[nt][i0 + 1][1] = hw[3];
       }
   }
 
   // Per-thread smem offsets inside a page (fixed for every page).
-  const int koff0 = r * 128 + ((cc ^ ((r & 1) << 2)) << 4);
-  const int koff1 = r * 128 + (((cc + 4) ^ ((r & 1) << 2)) << 4);
-  const int koff2 = koff0 + 8 * 128;  // row r+8 (same parity)
+  const int koff0 = r * 128 + ((c ^ ((r & 1) << 2)) << 4);         // token r, d [16c, 16c+16)
+  const int koff1 = r * 128 + (((c + 4) ^ ((r & 1) << 2)) << 4);   // token r, d [64+16c, ...)
+  const int koff2 = koff0 + 8 * 128;                                // token r+8 (same parity)
   const int koff3 = koff1 + 8 * 128;
-  const int R0 = 2 * cc, R1 = 2 * cc + 1;
-  const int voff0 = V_OFF + R0 * 128 + ((r ^ (R0 & 7)) << 4);        // tokens 2cc,2cc+1  d in [8r, 8r+8)
-  const int voff1 = V_OFF + R1 * 128 + ((r ^ (R1 & 7)) << 4);        // d in [64+8r, ...)
-  const int voff2 = V_OFF + (R0 + 8) * 128 + ((r ^ (R0 & 7)) << 4);  // tokens 8+2cc, 9+2cc
+  const int R0 = 2 * c, R1 = 2 * c + 1;
+  const int voff0 = V_OFF + R0 * 128 + ((r ^ (R0 & 7)) << 4);        // tokens 2c,2c+1 ; d [8r, 8r+8)
+  const int voff1 = V_OFF + R1 * 128 + ((r ^ (R1 & 7)) << 4);        // d [64+8r, 64+8r+8)
+  const int voff2 = V_OFF + (R0 + 8) * 128 + ((r ^ (R0 & 7)) << 4);  // tokens 8+2c, 9+2c
   const int voff3 = V_OFF + (R1 + 8) * 128 + ((r ^ (R1 & 7)) << 4);
 
-  float o[16][4];
+  // O^T accumulators: o[nt][mt] : c0 = (d = DA, head 2c), c1 = (DA, 2c+1),
+  // c2 = (DA+1, 2c), c3 = (DA+1, 2c+1); DA = (mt < 4 ? 8r + 2mt : 64 + 8r + 2(mt-4)).
+  float o[NT][8][4];
 #pragma unroll
-  for (int i = 0; i < 16; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.0f;
-  float m_lo = -INFINITY, m_hi = -INFINITY, l_lo = 0.0f, l_hi = 0.0f;
+  for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+    for (int i = 0; i < 8; ++i) o[nt][i][0] = o[nt][i][1] = o[nt][i][2] = o[nt][i][3] = 0.0f;
+  // Softmax state for heads 8nt + 2c + e (e = 0, 1); l is this thread's partial sum.
+  float m[NT][2], l[NT][2];
+  bool hvalid[NT][2];
+#pragma unroll
+  for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      m[nt][e] = -INFINITY;
+      l[nt][e] = 0.0f;
+      hvalid[nt][e] = 8 * nt + 2 * c + e < g;
+    }
   float escale = 1.0f;  // V-scale normaliser 2^E (fp16 range guard for P')
   bool escale_set = false;
 
@@ -425,67 +468,69 @@ __global__ void __launch_bounds__(THREADS, CTAS_PER_SM) decode_kernel(const Deco
     const uint4 k2 = lds128(pg + koff2), k3 = lds128(pg + koff3);
     const uint4 v0 = lds128(pg + voff0), v1 = lds128(pg + voff1);
     const uint4 v2 = lds128(pg + voff2), v3 = lds128(pg + voff3);
-    const float2 ks0 = lds64f(pg + KS_OFF + 8 * cc), ks1 = lds64f(pg + KS_OFF + 32 + 8 * cc);
-    float2 vs0 = lds64f(pg + VS_OFF + 8 * cc), vs1 = lds64f(pg + VS_OFF + 32 + 8 * cc);
+    float ks_r = lds32f(pg + KS_OFF + 4 * r), ks_r8 = lds32f(pg + KS_OFF + 32 + 4 * r);
+    float vs_r = lds32f(pg + VS_OFF + 4 * r), vs_r8 = lds32f(pg + VS_OFF + 32 + 4 * r);
 
-    // ---- S^T tile: rows = heads (r, r+8), cols = tokens (n-tile 0: 0..7, 1: 8..15);
-    //      two accumulator sets per n-tile halve the dependent-MMA chain.
-    float sc[2][4], sd[2][4];
+    // ---- S^T = K . Q^T : two accumulator chains per n-tile (k-steps 0-3, 4-7)
+    float sa[NT][4], sb[NT][4];
 #pragma unroll
-    for (int nt = 0; nt < 2; ++nt)
+    for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
-      for (int e = 0; e < 4; ++e) sc[nt][e] = sd[nt][e] = 0.0f;
+      for (int e = 0; e < 4; ++e) sa[nt][e] = sb[nt][e] = 0.0f;
     {
-      const uint32_t kw[2][8] = {{k0.x, k0.y, k0.z, k0.w, k1.x, k1.y, k1.z, k1.w},
-                                 {k2.x, k2.y, k2.z, k2.w, k3.x, k3.y, k3.z, k3.w}};
+      const uint32_t kr[8] = {k0.x, k0.y, k0.z, k0.w, k1.x, k1.y, k1.z, k1.w};
+      const uint32_t kr8[8] = {k2.x, k2.y, k2.z, k2.w, k3.x, k3.y, k3.z, k3.w};
 #pragma unroll
-      for (int i = 0; i < 8; ++i)
+      for (int i = 0; i < 8; ++i) {
+        uint32_t a0, a2, a1, a3;
+        codes_to_f16x2<KVD>(kr[i], a0, a2);
+        codes_to_f16x2<KVD>(kr8[i], a1, a3);
 #pragma unroll
-        for (int nt = 0; nt < 2; ++nt) {
-          uint32_t b0, b1;
-          codes_to_f16x2<KVD>(kw[nt][i], b0, b1);
-          mma16816(i < 4 ? sc[nt] : sd[nt], qlo[i][0], HI ? qhi[i][0] : 0u, qlo[i][1],
-                   HI ? qhi[i][1] : 0u, b0, b1);
-        }
+        for (int nt = 0; nt < NT; ++nt)
+          mma16816(i < 4 ? sa[nt] : sb[nt], a0, a1, a2, a3, qf[nt][i][0], qf[nt][i][1]);
+      }
     }
-    // ---- scores (log2 units) + masking of the tail page
+    // ---- scores in log2 units; thread holds tokens r, r+8 x heads 2c, 2c+1 per n-tile
     const int tok_base = (pg0 + warp + j * NW) * BS;
     const bool tail = tok_base + BS > L;
-    const float kscl[4] = {ks0.x * qscale, ks0.y * qscale, ks1.x * qscale, ks1.y * qscale};
-    float s_lo[4] = {(sc[0][0] + sd[0][0]) * kscl[0], (sc[0][1] + sd[0][1]) * kscl[1],
-                     (sc[1][0] + sd[1][0]) * kscl[2], (sc[1][1] + sd[1][1]) * kscl[3]};
-    float s_hi[4] = {(sc[0][2] + sd[0][2]) * kscl[0], (sc[0][3] + sd[0][3]) * kscl[1],
-                     (sc[1][2] + sd[1][2]) * kscl[2], (sc[1][3] + sd[1][3]) * kscl[3]};
-    if (tail) {
-      const int tk[4] = {2 * cc, 2 * cc + 1, 8 + 2 * cc, 9 + 2 * cc};
+    const bool ok_r = !tail || tok_base + r < L, ok_r8 = !tail || tok_base + r + 8 < L;
+    if (!ok_r) vs_r = 0.0f;
+    if (!ok_r8) vs_r8 = 0.0f;
+    const float kq_r = ks_r * qscale, kq_r8 = ks_r8 * qscale;
+    float sc[NT][4];  // [0]=(r,2c) [1]=(r,2c+1) [2]=(r+8,2c) [3]=(r+8,2c+1)
+    float mx[NT][2];
 #pragma unroll
-      for (int e = 0; e < 4; ++e)
-        if (tok_base + tk[e] >= L) {
-          s_lo[e] = -INFINITY;
-          s_hi[e] = -INFINITY;
-        }
-      if (tok_base + 2 * cc >= L) vs0.x = 0.0f;
-      if (tok_base + 2 * cc + 1 >= L) vs0.y = 0.0f;
-      if (tok_base + 8 + 2 * cc >= L) vs1.x = 0.0f;
-      if (tok_base + 9 + 2 * cc >= L) vs1.y = 0.0f;
+    for (int nt = 0; nt < NT; ++nt) {
+      sc[nt][0] = ok_r ? (sa[nt][0] + sb[nt][0]) * kq_r : -INFINITY;
+      sc[nt][1] = ok_r ? (sa[nt][1] + sb[nt][1]) * kq_r : -INFINITY;
+      sc[nt][2] = ok_r8 ? (sa[nt][2] + sb[nt][2]) * kq_r8 : -INFINITY;
+      sc[nt][3] = ok_r8 ? (sa[nt][3] + sb[nt][3]) * kq_r8 : -INFINITY;
+      mx[nt][0] = fmaxf(sc[nt][0], sc[nt][2]);
+      mx[nt][1] = fmaxf(sc[nt][1], sc[nt][3]);
     }
-    if (!row_lo_valid) s_lo[0] = s_lo[1] = s_lo[2] = s_lo[3] = 0.0f;
-    if (!row_hi_valid) s_hi[0] = s_hi[1] = s_hi[2] = s_hi[3] = 0.0f;
-    float mx_lo = fmaxf(fmaxf(s_lo[0], s_lo[1]), fmaxf(s_lo[2], s_lo[3]));
-    float mx_hi = fmaxf(fmaxf(s_hi[0], s_hi[1]), fmaxf(s_hi[2], s_hi[3]));
-    float vmax = fmaxf(fmaxf(vs0.x, vs0.y), fmaxf(vs1.x, vs1.y));
+    float vmax = fmaxf(vs_r, vs_r8);
 #pragma unroll
-    for (int o2 = 1; o2 <= 2; o2 <<= 1) {
-      mx_lo = fmaxf(mx_lo, __shfl_xor_sync(FULL, mx_lo, o2));
-      if (HI) mx_hi = fmaxf(mx_hi, __shfl_xor_sync(FULL, mx_hi, o2));
+    for (int o2 = 4; o2 <= 16; o2 <<= 1) {
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) {
+        mx[nt][0] = fmaxf(mx[nt][0], __shfl_xor_sync(FULL, mx[nt][0], o2));
+        mx[nt][1] = fmaxf(mx[nt][1], __shfl_xor_sync(FULL, mx[nt][1], o2));
+      }
       vmax = fmaxf(vmax, __shfl_xor_sync(FULL, vmax, o2));
     }
     // ---- lazy rescale (threshold 2^8 for p, [2^-10, 2^4] for the V normaliser)
-    const bool need_lo = row_lo_valid && mx_lo > m_lo + 8.0f;
-    const bool need_hi = row_hi_valid && mx_hi > m_hi + 8.0f;
+    bool need = false;
+    bool nm[NT][2];
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        nm[nt][e] = hvalid[nt][e] && mx[nt][e] > m[nt][e] + 8.0f;
+        need |= nm[nt][e];
+      }
     const float ve = vmax * escale;
     const bool need_e = vmax > 0.0f && (!escale_set || ve > 16.0f || ve < 0.0009765625f);
-    if (__any_sync(FULL, need_lo || need_hi || need_e)) {
+    if (__any_sync(FULL, need || need_e)) {
       float e_new = escale;
       if (need_e) {
         int ex;
@@ -494,64 +539,65 @@ __global__ void __launch_bounds__(THREADS, CTAS_PER_SM) decode_kernel(const Deco
         escale_set = true;
       }
       const float er = e_new / escale;  // exact power of two
-      const float mn_lo = need_lo ? mx_lo : m_lo;
-      const float mn_hi = need_hi ? mx_hi : m_hi;
-      const float c_lo = need_lo ? fast_exp2(m_lo - mn_lo) : 1.0f;
-      const float c_hi = need_hi ? fast_exp2(m_hi - mn_hi) : 1.0f;
-      l_lo *= c_lo;
-      l_hi *= c_hi;
-      const float f_lo = c_lo * er, f_hi = c_hi * er;
+      escale = e_new;
 #pragma unroll
-      for (int i = 0; i < 16; ++i) {
-        o[i][0] *= f_lo;
-        o[i][1] *= f_lo;
-        if (HI) {
-          o[i][2] *= f_hi;
-          o[i][3] *= f_hi;
+      for (int nt = 0; nt < NT; ++nt) {
+        float f[2];
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const float cl = nm[nt][e] ? fast_exp2(m[nt][e] - mx[nt][e]) : 1.0f;
+          if (nm[nt][e]) m[nt][e] = mx[nt][e];
+          l[nt][e] *= cl;
+          f[e] = cl * er;
+        }
+#pragma unroll
+        for (int mt = 0; mt < 8; ++mt) {
+          o[nt][mt][0] *= f[0];
+          o[nt][mt][1] *= f[1];
+          o[nt][mt][2] *= f[0];
+          o[nt][mt][3] *= f[1];
         }
       }
-      m_lo = mn_lo;
-      m_hi = mn_hi;
-      escale = e_new;
     }
-    // ---- probabilities: p (fp32, for l) and P' = p * scale_v * 2^E (fp16, for PV)
-    const float w[4] = {vs0.x * escale, vs0.y * escale, vs1.x * escale, vs1.y * escale};
-    float p_lo[4], p_hi[4];
+    // ---- p (fp32, for l) and P' = p * scale_v * 2^E (fp16) -> P'^T B-fragments
+    const float w_r = vs_r * escale, w_r8 = vs_r8 * escale;
+    uint32_t pb[NT][2];
 #pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      p_lo[e] = row_lo_valid ? fast_exp2(s_lo[e] - m_lo) : 0.0f;
-      p_hi[e] = row_hi_valid ? fast_exp2(s_hi[e] - m_hi) : 0.0f;
-      l_lo += p_lo[e];
-      l_hi += p_hi[e];
-    }
-    const uint32_t pa0 = pack_half2(p_lo[0] * w[0], p_lo[1] * w[1]);
-    const uint32_t pa2 = pack_half2(p_lo[2] * w[2], p_lo[3] * w[3]);
-    const uint32_t pa1 = HI ? pack_half2(p_hi[0] * w[0], p_hi[1] * w[1]) : 0u;
-    const uint32_t pa3 = HI ? pack_half2(p_hi[2] * w[2], p_hi[3] * w[3]) : 0u;
-
-    // ---- O += P' V : n-tile nt <-> d = (nt < 8 ? 8r + nt : 64 + 8r + nt - 8) for B column r
-    const uint32_t vw[2][8] = {{v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w},
-                               {v2.x, v2.y, v2.z, v2.w, v3.x, v3.y, v3.z, v3.w}};
-    uint32_t vmask0 = 0xffffffffu, vmask1 = 0xffffffffu;
-    if (KVD == KVQ_FP8_E4M3 && tail) {  // garbage E4M3 codes may be NaN: zero masked tokens
-      vmask0 = (tok_base + 2 * cc < L ? 0x0000ffffu : 0u) | (tok_base + 2 * cc + 1 < L ? 0xffff0000u : 0u);
-      vmask1 = (tok_base + 8 + 2 * cc < L ? 0x0000ffffu : 0u) | (tok_base + 9 + 2 * cc < L ? 0xffff0000u : 0u);
-    }
+    for (int nt = 0; nt < NT; ++nt) {
+      float pv[4];
 #pragma unroll
-    for (int jj = 0; jj < 8; ++jj) {
-      uint32_t b0a, b0b, b1a, b1b;
-      codes_to_f16x2<KVD>(vw[0][jj], b0a, b0b);
-      codes_to_f16x2<KVD>(vw[1][jj], b1a, b1b);
-      if (KVD == KVQ_FP8_E4M3) {
-        b0a &= vmask0;
-        b0b &= vmask0;
-        b1a &= vmask1;
-        b1b &= vmask1;
+      for (int q4 = 0; q4 < 4; ++q4) {
+        const int e = q4 & 1;
+        pv[q4] = hvalid[nt][e] ? fast_exp2(sc[nt][q4] - m[nt][e]) : 0.0f;
+        l[nt][e] += pv[q4];
       }
-      // word jj of a chunk -> d pair (2jj, 2jj+1) within its 8-wide d range -> n-tiles
-      const int nt0 = (jj < 4) ? 2 * jj : 8 + 2 * (jj - 4);
-      mma16816(o[nt0], pa0, pa1, pa2, pa3, b0a, b1a);
-      mma16816(o[nt0 + 1], pa0, pa1, pa2, pa3, b0b, b1b);
+      // 8x8 blocks: rows = tokens (r | r+8), cols = heads (2c, 2c+1)
+      const uint32_t x0 = pack_half2(pv[0] * w_r, pv[1] * w_r);
+      const uint32_t x1 = pack_half2(pv[2] * w_r8, pv[3] * w_r8);
+      pb[nt][0] = movmatrix_trans(x0);  // (tokens 2c, 2c+1 ; head r)
+      pb[nt][1] = movmatrix_trans(x1);  // (tokens 8+2c, 9+2c ; head r)
+    }
+    // ---- O^T += V^T . P'^T
+    const uint32_t va[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};  // tokens 2c, 2c+1
+    const uint32_t vb[8] = {v2.x, v2.y, v2.z, v2.w, v3.x, v3.y, v3.z, v3.w};  // tokens 8+2c, 9+2c
+    uint32_t vmask_a = 0xffffffffu, vmask_b = 0xffffffffu;
+    if (KVD == KVQ_FP8_E4M3 && tail) {  // garbage E4M3 codes may be NaN: zero masked tokens
+      vmask_a = (tok_base + 2 * c < L ? 0x0000ffffu : 0u) | (tok_base + 2 * c + 1 < L ? 0xffff0000u : 0u);
+      vmask_b = (tok_base + 8 + 2 * c < L ? 0x0000ffffu : 0u) | (tok_base + 9 + 2 * c < L ? 0xffff0000u : 0u);
+    }
+#pragma unroll
+    for (int mt = 0; mt < 8; ++mt) {
+      uint32_t a0, a1, a2, a3;
+      codes_to_f16x2<KVD>(va[mt], a0, a1);  // (DA, tok 2c|2c+1), (DA+1, ...)
+      codes_to_f16x2<KVD>(vb[mt], a2, a3);  // (DA, tok 8+2c|9+2c), (DA+1, ...)
+      if (KVD == KVQ_FP8_E4M3) {
+        a0 &= vmask_a;
+        a1 &= vmask_a;
+        a2 &= vmask_b;
+        a3 &= vmask_b;
+      }
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) mma16816(o[nt][mt], a0, a1, a2, a3, pb[nt][0], pb[nt][1]);
     }
     // ---- refill this slot with page j + S (its smem was fully consumed above)
     if (j + S < ps.nj) {
@@ -562,40 +608,43 @@ __global__ void __launch_bounds__(THREADS, CTAS_PER_SM) decode_kernel(const Deco
   }
 
   // ===== CTA merge of the NW warps =====
-  l_lo += __shfl_xor_sync(FULL, l_lo, 1);
-  l_lo += __shfl_xor_sync(FULL, l_lo, 2);
-  l_hi += __shfl_xor_sync(FULL, l_hi, 1);
-  l_hi += __shfl_xor_sync(FULL, l_hi, 2);
+#pragma unroll
+  for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+    for (int e = 0; e < 2; ++e)
+#pragma unroll
+      for (int o2 = 4; o2 <= 16; o2 <<= 1) l[nt][e] += __shfl_xor_sync(FULL, l[nt][e], o2);
   __syncthreads();  // every ring slot consumed: reuse smem as merge scratch
-  float* so = reinterpret_cast<float*>(smem);  // [NW][16][128]
+  float* so = reinterpret_cast<float*>(smem);  // [NW][16 heads][128]
   float* sm = so + NW * 16 * HD;               // [NW][16] m
   float* sl = sm + NW * 16;                    // [NW][16] l
-  if (cc == 0) {
-    sm[warp * 16 + r] = row_lo_valid ? m_lo : -INFINITY;
-    sl[warp * 16 + r] = l_lo;
-    sm[warp * 16 + r + 8] = row_hi_valid ? m_hi : -INFINITY;
-    sl[warp * 16 + r + 8] = l_hi;
+  if (r == 0) {
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        sm[warp * 16 + 8 * nt + 2 * c + e] = hvalid[nt][e] ? m[nt][e] : -INFINITY;
+        sl[warp * 16 + 8 * nt + 2 * c + e] = l[nt][e];
+      }
   }
   __syncthreads();
-  {
-    float M_lo = -INFINITY, M_hi = -INFINITY;
 #pragma unroll
-    for (int w2 = 0; w2 < NW; ++w2) {
-      M_lo = fmaxf(M_lo, sm[w2 * 16 + r]);
-      M_hi = fmaxf(M_hi, sm[w2 * 16 + r + 8]);
+  for (int nt = 0; nt < NT; ++nt) {
+    float f[2];
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int hh = 8 * nt + 2 * c + e;
+      float M = -INFINITY;
+#pragma unroll
+      for (int w2 = 0; w2 < NW; ++w2) M = fmaxf(M, sm[w2 * 16 + hh]);
+      f[e] = (hvalid[nt][e] && m[nt][e] > -INFINITY) ? fast_exp2(m[nt][e] - M) / escale : 0.0f;
     }
-    const float f_lo = (row_lo_valid && m_lo > -INFINITY) ? fast_exp2(m_lo - M_lo) / escale : 0.0f;
-    const float f_hi = (row_hi_valid && m_hi > -INFINITY) ? fast_exp2(m_hi - M_hi) / escale : 0.0f;
-    float* mine = so + warp * 16 * HD;
+    float* mine = so + (warp * 16 + 8 * nt + 2 * c) * HD;
 #pragma unroll
-    for (int nt = 0; nt < 16; ++nt) {
-      const int d0 = (nt < 8 ? 16 * cc + nt : 64 + 16 * cc + (nt - 8));
-      mine[r * HD + d0] = o[nt][0] * f_lo;
-      mine[r * HD + d0 + 8] = o[nt][1] * f_lo;
-      if (HI) {
-        mine[(r + 8) * HD + d0] = o[nt][2] * f_hi;
-        mine[(r + 8) * HD + d0 + 8] = o[nt][3] * f_hi;
-      }
+    for (int mt = 0; mt < 8; ++mt) {
+      const int da = (mt < 4 ? 8 * r + 2 * mt : 64 + 8 * r + 2 * (mt - 4));
+      *reinterpret_cast<float2*>(mine + da) = make_float2(o[nt][mt][0] * f[0], o[nt][mt][2] * f[0]);
+      *reinterpret_cast<float2*>(mine + HD + da) = make_float2(o[nt][mt][1] * f[1], o[nt][mt][3] * f[1]);
     }
   }
   __syncthreads();
@@ -608,15 +657,12 @@ __global__ void __launch_bounds__(THREADS, CTAS_PER_SM) decode_kernel(const Deco
 #pragma unroll
     for (int w2 = 0; w2 < NW; ++w2) M = fmaxf(M, sm[w2 * 16 + row]);
     float lsum = 0.0f;
-#pragma unroll
-    for (int w2 = 0; w2 < NW; ++w2) {
-      const float mw = sm[w2 * 16 + row];
-      if (mw > -INFINITY) lsum += sl[w2 * 16 + row] * fast_exp2(mw - M);
-    }
     float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
 #pragma unroll
     for (int w2 = 0; w2 < NW; ++w2) {
-      if (sm[w2 * 16 + row] == -INFINITY) continue;  // warp saw no page
+      const float mw = sm[w2 * 16 + row];
+      if (mw == -INFINITY) continue;  // warp saw no page
+      lsum += sl[w2 * 16 + row] * fast_exp2(mw - M);
       const float* src = so + (w2 * 16 + row) * HD + d0;
 #pragma unroll
       for (int e = 0; e < 8; ++e) acc[e] += src[e];
@@ -659,15 +705,15 @@ __global__ void __launch_bounds__(THREADS, CTAS_PER_SM) decode_kernel(const Deco
       const float wgt = fast_exp2(__ldcg(p.part_lse + base + sp) - M);
       wsum += wgt;
       const float4 a = __ldcg(reinterpret_cast<const float4*>(p.part_o + (base + sp) * HD + d0));
-      const float4 c = __ldcg(reinterpret_cast<const float4*>(p.part_o + (base + sp) * HD + d0 + 4));
+      const float4 cc = __ldcg(reinterpret_cast<const float4*>(p.part_o + (base + sp) * HD + d0 + 4));
       acc[0] += wgt * a.x;
       acc[1] += wgt * a.y;
       acc[2] += wgt * a.z;
       acc[3] += wgt * a.w;
-      acc[4] += wgt * c.x;
-      acc[5] += wgt * c.y;
-      acc[6] += wgt * c.z;
-      acc[7] += wgt * c.w;
+      acc[4] += wgt * cc.x;
+      acc[5] += wgt * cc.y;
+      acc[6] += wgt * cc.z;
+      acc[7] += wgt * cc.w;
     }
     const float inv = 1.0f / wsum;
 #pragma unroll
@@ -838,14 +884,15 @@ int kvq_decode_attn(const void* q, int64_t q_batch_stride, const void* pool, int
   const dim3 grid((unsigned)max_splits, (unsigned)Hkv, (unsigned)B);
   auto st = static_cast<cudaStream_t>(stream);
   const bool hi = prm.g > 8;
+  const size_t smem_bytes = hi ? kvq::Geo<true>::SMEM : kvq::Geo<false>::SMEM;
   auto launch = [&](auto kernel) -> int {
     cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)kvq::DECODE_SMEM);
+                                         (int)smem_bytes);
     if (e == cudaSuccess)
       e = cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
                                cudaSharedmemCarveoutMaxShared);
     if (e != cudaSuccess) return fail(KVQ_ECUDA, cudaGetErrorString(e));
-    kernel<<<grid, kvq::THREADS, kvq::DECODE_SMEM, st>>>(prm);
+    kernel<<<grid, kvq::THREADS, smem_bytes, st>>>(prm);
     return check_launch("decode_attn");
   };
   if (kv_dtype == KVQ_INT8)

@@ -284,22 +284,14 @@ def run_ours(args, cfg):
     k_new = torch.randn((B, Hkv, 128), device=dev, generator=gen).to(torch.bfloat16)[:, kv0:kv1].contiguous()
     v_new = torch.randn((B, Hkv, 128), device=dev, generator=gen).to(torch.bfloat16)[:, kv0:kv1].contiguous()
     total_pages = int(nblk.sum())
-    out_loc = torch.empty((Hq_loc, B, 128), dtype=torch.bfloat16, device=dev)
-    out_all = torch.empty((Hq, B, 128), dtype=torch.bfloat16, device=dev) if world > 1 else out_loc
 
-    def attention():
-        return paged_decode_attention(q, cache, table_d, seq_lens_d, out=out_loc, head_major=True,
-                                      total_pages=total_pages)
-
-    def step(ev=None):
-        quantize_append(cache, k_new, v_new, slots_step)
-        if ev is not None:
-            ev[0].record()
-        attention()
-        if ev is not None:
-            ev[1].record()
-        if world > 1:
-            dist.all_gather_into_tensor(out_all, out_loc)
+    from paper_2605_29639_b200.session import DecodeSession
+    sess = DecodeSession(cache, table_d, B, Hq_loc, total_pages=total_pages, head_major=True,
+                         gather_group=dist.group.WORLD if world > 1 else None, world=world)
+    buf = sess.device_buffers(0)
+    for name, t in (("q", q), ("k", k_new), ("v", v_new), ("slots", slots_step), ("lens", seq_lens_d)):
+        buf[name].copy_(t)
+    out_all = torch.empty((Hq, B, 128), dtype=torch.bfloat16, device=dev) if world > 1 else None
 
     def barrier():
         if world > 1:
@@ -313,11 +305,24 @@ def run_ours(args, cfg):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
+    # ---- device-resident timed region: CUDA-graph replays of K1 and K2 ------
+    sess._kernels(buf)  # warm the kernels (and lazy module loading) before capture
+    torch.cuda.synchronize()
+    g_append, g_attn = sess.capture()
+
+    def step(ev=None):
+        g_append.replay()
+        if ev is not None:
+            ev[0].record()
+        g_attn.replay()
+        if ev is not None:
+            ev[1].record()
+        if world > 1:
+            dist.all_gather_into_tensor(out_all, buf["out"])
+
     for _ in range(args.warmup):
         step()
     barrier()
-
-    # ---- device-resident timed region --------------------------------------
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
            for _ in range(args.steps)]
     t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -334,41 +339,30 @@ def run_ours(args, cfg):
     k2_ms = statistics.mean(a.elapsed_time(b) for a, b in evs)
     k2_ms = max_over_ranks(k2_ms)
 
-    # ---- end-to-end through the public API with host buffers ----------------
-    pin = dict(pin_memory=True)
+    # ---- end-to-end through the public API with pinned host buffers ----------
     q_h = q.cpu().pin_memory()
     k_h, v_h = k_new.cpu().pin_memory(), v_new.cpu().pin_memory()
     slots_h = slots_step.cpu().pin_memory()
     lens_h = seq_lens_d.cpu().pin_memory()
-    o_h = torch.empty(tuple(out_all.shape), dtype=torch.bfloat16, **pin)
-    q_d, k_d, v_d = torch.empty_like(q), torch.empty_like(k_new), torch.empty_like(v_new)
-    slots_d, lens_d = torch.empty_like(slots_step), torch.empty_like(seq_lens_d)
+    o_h = torch.empty((Hq, B, 128), dtype=torch.bfloat16, pin_memory=True)
 
     def e2e_step():
-        q_d.copy_(q_h, non_blocking=True)
-        k_d.copy_(k_h, non_blocking=True)
-        v_d.copy_(v_h, non_blocking=True)
-        slots_d.copy_(slots_h, non_blocking=True)
-        lens_d.copy_(lens_h, non_blocking=True)
-        quantize_append(cache, k_d, v_d, slots_d)
-        paged_decode_attention(q_d, cache, table_d, lens_d, out=out_loc, head_major=True,
-                               total_pages=total_pages)
-        if world > 1:
-            dist.all_gather_into_tensor(out_all, out_loc)
-        o_h.copy_(out_all, non_blocking=True)
+        sess.submit(q_h, k_h, v_h, slots_h, lens_h, o_h)
 
     for _ in range(args.warmup):
         e2e_step()
+    sess.synchronize()
     barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
+    e0.record(sess.h2d)
     for _ in range(args.steps):
         e2e_step()
-    e1.record()
+    e1.record(sess.d2h)
+    sess.synchronize()
     torch.cuda.synchronize()
     e2e_ms = max_over_ranks(e0.elapsed_time(e1)) / args.steps
     h2d = sum(t.numel() * t.element_size() for t in (q_h, k_h, v_h, slots_h, lens_h))
-    d2h = o_h.numel() * o_h.element_size() // (world if world > 1 else 1)
+    d2h = o_h.numel() * o_h.element_size()
 
     # ---- CPU baseline (rank 0, N = 1 only) -----------------------------------
     cpu = None
@@ -409,7 +403,10 @@ def run_ours(args, cfg):
                    "l2": "inputs larger than L2 (pool %.2f GB vs 126 MB L2); no flush" % (cache.nbytes() * world / 1e9)
                    if cache.nbytes() * world > 4 * 126e6 else "pool fits in L2: L2-resident numbers",
                    "step": "K1 append of B rows + K2 paged decode attention (+ all-gather if N>1); "
-                           "stationary ctx", "compute": "codes->f16 in registers, mma.sync f16 x f16 -> f32"},
+                           "stationary ctx; device steps replay CUDA graphs of K1 and K2",
+                   "e2e": "DecodeSession.submit: H2D of q/k/v/slots/lens from pinned memory, K1, K2, "
+                          "(all-gather), D2H of O; double-buffered copy streams overlap adjacent steps",
+                   "compute": "codes->f16 in registers, mma.sync m16n8k16 f16 x f16 -> f32"},
         "hbm_gbs_algorithmic_step": (attn_bytes + append_bytes) / (ms_step * 1e-3) / 1e9,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "kernel": "kvq::decode_kernel",

@@ -188,8 +188,10 @@ __device__ __forceinline__ float fast_exp2(float x) {
 }
 
 // 8-bit codes -> two f16x2 registers (exact for every INT8 / E4M3 code).
-// Input bytes (b0, b1, b2, b3) -> lo = (b0, b1), hi = (b2, b3).
-template <int KVD>
+// Input bytes (b0, b1, b2, b3) -> lo = (b0, b1), hi = (b2, b3).  With
+// BIASED (INT8 only) the values are code + 1152 and the caller removes the
+// bias after the MMA (saves two HSUB2 per word).
+template <int KVD, bool BIASED = false>
 __device__ __forceinline__ void codes_to_f16x2(uint32_t w, uint32_t& lo, uint32_t& hi) {
   if constexpr (KVD == KVQ_FP8_E4M3) {
     asm("{\n\t.reg .b16 l, h;\n\tmov.b32 {l, h}, %2;\n\t"
@@ -201,9 +203,11 @@ __device__ __forceinline__ void codes_to_f16x2(uint32_t w, uint32_t& lo, uint32_
     const uint32_t u = w ^ 0x80808080u;
     asm("prmt.b32 %0, %1, %2, 0x7170;" : "=r"(lo) : "r"(u), "r"(0x64646464u));
     asm("prmt.b32 %0, %1, %2, 0x7372;" : "=r"(hi) : "r"(u), "r"(0x64646464u));
-    const uint32_t magic = 0x64806480u;  // (1152, 1152)
-    asm("sub.f16x2 %0, %0, %1;" : "+r"(lo) : "r"(magic));
-    asm("sub.f16x2 %0, %0, %1;" : "+r"(hi) : "r"(magic));
+    if (!BIASED) {
+      const uint32_t magic = 0x64806480u;  // (1152, 1152)
+      asm("sub.f16x2 %0, %0, %1;" : "+r"(lo) : "r"(magic));
+      asm("sub.f16x2 %0, %0, %1;" : "+r"(hi) : "r"(magic));
+    }
   }
 }
 
@@ -298,8 +302,8 @@ struct PageStream {
     cur = load_ids(0, lane);
     nxt = nj > 32 ? load_ids(32, lane) : 0;
   }
-  // Issue the bulk copy of page j (j >= base, all lanes participate).
-  __device__ __forceinline__ void issue(int j, int lane) {
+  // Issue the bulk copy of page j into slot s (j >= base, all lanes participate).
+  __device__ __forceinline__ void issue(int j, int lane, int s) {
     if (j >= base + 32) {  // advance the id window (warp-uniform)
       base += 32;
       cur = nxt;
@@ -307,7 +311,6 @@ struct PageStream {
     }
     const int blk = __shfl_sync(FULL, cur, j - base);
     if (lane == 0) {
-      const int s = j % S;
       mbar_arrive_expect_tx(&full[s], PAGE);
       bulk_g2s(ring + s * PAGE, head_base + blk * blk_stride, PAGE, &full[s], policy);
     }
@@ -368,7 +371,7 @@ __global__ void __launch_bounds__(THREADS, Geo<HI>::CTAS) decode_kernel(const De
   __syncwarp();
   ps.init(lane);
 #pragma unroll 1
-  for (int j = 0; j < S && j < ps.nj; ++j) ps.issue(j, lane);
+  for (int j = 0; j < S && j < ps.nj; ++j) ps.issue(j, lane, j);
 
   const int r = lane >> 2, c = lane & 3;
 
@@ -426,6 +429,26 @@ __global__ void __launch_bounds__(THREADS, Geo<HI>::CTAS) decode_kernel(const De
         qf[nt][i0 + 1][1] = hw[3];
       }
   }
+  // INT8 K is fed to the MMA as code + 1152 (no HSUB2): S^T' = S^T + 1152 * sum_d q'.
+  // kbias[nt][e] = 1152 * sum_d q'[head 8nt + 2c + e][d], from the f16 values the MMA sees.
+  float kbias[NT][2];
+#pragma unroll
+  for (int nt = 0; nt < NT; ++nt) {
+    float qs = 0.0f;
+    if (KVD == KVQ_INT8) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&qf[nt][i][e]));
+          qs += f.x + f.y;
+        }
+      qs += __shfl_xor_sync(FULL, qs, 1);
+      qs += __shfl_xor_sync(FULL, qs, 2);
+    }
+#pragma unroll
+    for (int e = 0; e < 2; ++e) kbias[nt][e] = 1152.0f * __shfl_sync(FULL, qs, 4 * (2 * c + e));
+  }
 
   // Per-thread smem offsets inside a page (fixed for every page).
   const int koff0 = r * 128 + ((c ^ ((r & 1) << 2)) << 4);         // token r, d [16c, 16c+16)
@@ -459,11 +482,12 @@ __global__ void __launch_bounds__(THREADS, Geo<HI>::CTAS) decode_kernel(const De
   float escale = 1.0f;  // V-scale normaliser 2^E (fp16 range guard for P')
   bool escale_set = false;
 
+  int slot = 0;
+  uint32_t phase = 0;
 #pragma unroll 1
   for (int j = 0; j < ps.nj; ++j) {
-    const int s = j % S;
-    mbar_wait(&ps.full[s], (j / S) & 1);
-    const uint8_t* pg = ps.ring + s * PAGE;
+    mbar_wait(&ps.full[slot], phase);
+    const uint8_t* pg = ps.ring + slot * PAGE;
     const uint4 k0 = lds128(pg + koff0), k1 = lds128(pg + koff1);
     const uint4 k2 = lds128(pg + koff2), k3 = lds128(pg + koff3);
     const uint4 v0 = lds128(pg + voff0), v1 = lds128(pg + voff1);
@@ -483,8 +507,8 @@ __global__ void __launch_bounds__(THREADS, Geo<HI>::CTAS) decode_kernel(const De
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
         uint32_t a0, a2, a1, a3;
-        codes_to_f16x2<KVD>(kr[i], a0, a2);
-        codes_to_f16x2<KVD>(kr8[i], a1, a3);
+        codes_to_f16x2<KVD, true>(kr[i], a0, a2);
+        codes_to_f16x2<KVD, true>(kr8[i], a1, a3);
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt)
           mma16816(i < 4 ? sa[nt] : sb[nt], a0, a1, a2, a3, qf[nt][i][0], qf[nt][i][1]);
@@ -501,10 +525,10 @@ __global__ void __launch_bounds__(THREADS, Geo<HI>::CTAS) decode_kernel(const De
     float mx[NT][2];
 #pragma unroll
     for (int nt = 0; nt < NT; ++nt) {
-      sc[nt][0] = ok_r ? (sa[nt][0] + sb[nt][0]) * kq_r : -INFINITY;
-      sc[nt][1] = ok_r ? (sa[nt][1] + sb[nt][1]) * kq_r : -INFINITY;
-      sc[nt][2] = ok_r8 ? (sa[nt][2] + sb[nt][2]) * kq_r8 : -INFINITY;
-      sc[nt][3] = ok_r8 ? (sa[nt][3] + sb[nt][3]) * kq_r8 : -INFINITY;
+      sc[nt][0] = ok_r ? (sa[nt][0] + sb[nt][0] - kbias[nt][0]) * kq_r : -INFINITY;
+      sc[nt][1] = ok_r ? (sa[nt][1] + sb[nt][1] - kbias[nt][1]) * kq_r : -INFINITY;
+      sc[nt][2] = ok_r8 ? (sa[nt][2] + sb[nt][2] - kbias[nt][0]) * kq_r8 : -INFINITY;
+      sc[nt][3] = ok_r8 ? (sa[nt][3] + sb[nt][3] - kbias[nt][1]) * kq_r8 : -INFINITY;
       mx[nt][0] = fmaxf(sc[nt][0], sc[nt][2]);
       mx[nt][1] = fmaxf(sc[nt][1], sc[nt][3]);
     }
@@ -599,11 +623,16 @@ __global__ void __launch_bounds__(THREADS, Geo<HI>::CTAS) decode_kernel(const De
 #pragma unroll
       for (int nt = 0; nt < NT; ++nt) mma16816(o[nt][mt], a0, a1, a2, a3, pb[nt][0], pb[nt][1]);
     }
-    // ---- refill this slot with page j + S (its smem was fully consumed above)
+    // ---- refill this slot with page j + S.  Every LDS of the slot has
+    // returned (its registers were consumed by the MMAs above) in every lane
+    // (__syncwarp), so the async-proxy overwrite cannot race the reads.
     if (j + S < ps.nj) {
       __syncwarp();
-      if (lane == 0) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      ps.issue(j + S, lane);
+      ps.issue(j + S, lane, slot);
+    }
+    if (++slot == S) {
+      slot = 0;
+      phase ^= 1;
     }
   }
 

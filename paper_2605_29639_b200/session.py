@@ -1,0 +1,132 @@
+"""Host-side decode-step runtime: one attention layer's decode step for a fixed
+batch, from pinned host buffers to pinned host buffers.
+
+    sess = DecodeSession(cache, block_table, batch=B, num_q_heads=Hq)
+    sess.submit(q_h, k_h, v_h, slots_h, lens_h, out_h)   # async, returns an event
+    ...
+    sess.synchronize()
+
+Each step uploads its inputs (q, the new K/V rows, slot mapping, sequence
+lengths) on a copy stream, runs K1 (quantize-on-append) + K2 (paged decode
+attention) on the compute stream and downloads the output on a second copy
+stream.  Device buffers are double-buffered, so step i+1's uploads and step
+i-1's download overlap step i's kernels; stream-ordering events make every
+reuse safe.  This is the serving-loop counterpart of the reference's
+``_on_decode_step`` (simulator.py:504-517), with the KV write of the decoded
+token that the reference never models.
+
+``capture()`` returns CUDA graphs of the device part of one step (K1, K2) over
+the session's own device buffers, for launch-bound small batches.
+"""
+from __future__ import annotations
+
+from typing import List, Optional
+
+import torch
+
+from . import _lib
+from .cache import PagedKVCache
+from .ops import paged_decode_attention, quantize_append, workspace_bytes
+
+
+class DecodeSession:
+    def __init__(self, cache: PagedKVCache, block_table: torch.Tensor, batch: int, num_q_heads: int,
+                 *, total_pages: Optional[int] = None, out_dtype: torch.dtype = torch.bfloat16,
+                 head_major: bool = False, sm_scale: Optional[float] = None, depth: int = 2,
+                 gather_group=None, world: int = 1):
+        """With ``gather_group`` (KV-head sharding, paper_2605_29639_b200.shard)
+        the local head-major output ``[Hq/P, B, d]`` is all-gathered into
+        ``[Hq, B, d]`` on the compute stream before the download."""
+        dev = cache.device
+        self.gather_group, self.world = gather_group, world
+        if gather_group is not None:
+            head_major = True
+        self.cache, self.block_table = cache, block_table
+        self.B, self.Hq, self.Hkv = batch, num_q_heads, cache.spec.num_kv_heads
+        self.head_major, self.sm_scale, self.out_dtype = head_major, sm_scale, out_dtype
+        lib = _lib.load()
+        max_blocks = block_table.shape[1]
+        self.pps = int(lib.kvq_decode_pages_per_split(
+            batch, self.Hkv, total_pages if total_pages is not None else batch * max_blocks, max_blocks))
+        max_splits = -(-max_blocks // self.pps)
+        self.depth = depth
+        self.compute = torch.cuda.current_stream(dev)
+        self.h2d = torch.cuda.Stream(dev)
+        self.d2h = torch.cuda.Stream(dev)
+        oshape = (num_q_heads, batch, 128) if head_major else (batch, num_q_heads, 128)
+        self.bufs = []
+        for _ in range(depth):
+            self.bufs.append(dict(
+                q=torch.empty((batch, num_q_heads, 128), dtype=torch.bfloat16, device=dev),
+                k=torch.empty((batch, self.Hkv, 128), dtype=torch.bfloat16, device=dev),
+                v=torch.empty((batch, self.Hkv, 128), dtype=torch.bfloat16, device=dev),
+                slots=torch.empty((batch,), dtype=torch.int32, device=dev),
+                lens=torch.empty((batch,), dtype=torch.int32, device=dev),
+                out=torch.empty(oshape, dtype=out_dtype, device=dev),
+                out_all=(torch.empty((num_q_heads * world, batch, 128), dtype=out_dtype, device=dev)
+                         if gather_group is not None else None),
+                ws=torch.zeros(workspace_bytes(batch, num_q_heads, self.Hkv, max_splits),
+                               dtype=torch.uint8, device=dev),
+                in_ready=torch.cuda.Event(), done=torch.cuda.Event(), out_done=torch.cuda.Event(),
+                used=False))
+        self.step_idx = 0
+
+    def _kernels(self, buf) -> None:
+        quantize_append(self.cache, buf["k"], buf["v"], buf["slots"])
+        paged_decode_attention(buf["q"], self.cache, self.block_table, buf["lens"], out=buf["out"],
+                               head_major=self.head_major, sm_scale=self.sm_scale,
+                               pages_per_split=self.pps, out_dtype=self.out_dtype,
+                               workspace=buf["ws"])
+
+    def submit(self, q_h: torch.Tensor, k_h: torch.Tensor, v_h: torch.Tensor, slots_h: torch.Tensor,
+               lens_h: torch.Tensor, out_h: torch.Tensor) -> torch.cuda.Event:
+        """Enqueue one decode step.  Host tensors should be pinned; they must
+        stay untouched until the returned event completes."""
+        buf = self.bufs[self.step_idx % self.depth]
+        self.step_idx += 1
+        with torch.cuda.stream(self.h2d):
+            if buf["used"]:
+                self.h2d.wait_event(buf["done"])      # previous kernels finished reading
+            buf["q"].copy_(q_h, non_blocking=True)
+            buf["k"].copy_(k_h, non_blocking=True)
+            buf["v"].copy_(v_h, non_blocking=True)
+            buf["slots"].copy_(slots_h, non_blocking=True)
+            buf["lens"].copy_(lens_h, non_blocking=True)
+            buf["in_ready"].record(self.h2d)
+        self.compute.wait_event(buf["in_ready"])
+        if buf["used"]:
+            self.compute.wait_event(buf["out_done"])   # previous download of this out buffer
+        with torch.cuda.stream(self.compute):
+            self._kernels(buf)
+            if self.gather_group is not None:
+                import torch.distributed as dist
+                dist.all_gather_into_tensor(buf["out_all"], buf["out"], group=self.gather_group)
+        buf["done"].record(self.compute)
+        with torch.cuda.stream(self.d2h):
+            self.d2h.wait_event(buf["done"])
+            out_h.copy_(buf["out_all"] if self.gather_group is not None else buf["out"], non_blocking=True)
+            buf["out_done"].record(self.d2h)
+        buf["used"] = True
+        return buf["out_done"]
+
+    def synchronize(self) -> None:
+        for s in (self.h2d, self.compute, self.d2h):
+            s.synchronize()
+
+    def capture(self) -> List[torch.cuda.CUDAGraph]:
+        """CUDA graphs [K1, K2] of one step over device buffer 0's contents."""
+        buf = self.bufs[0]
+        graphs = []
+        for fn in (lambda: quantize_append(self.cache, buf["k"], buf["v"], buf["slots"]),
+                   lambda: paged_decode_attention(
+                       buf["q"], self.cache, self.block_table, buf["lens"], out=buf["out"],
+                       head_major=self.head_major, sm_scale=self.sm_scale, pages_per_split=self.pps,
+                       out_dtype=self.out_dtype, workspace=buf["ws"])):
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                fn()
+            graphs.append(g)
+        return graphs
+
+    def device_buffers(self, i: int = 0) -> dict:
+        return self.bufs[i]

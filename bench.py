@@ -46,6 +46,10 @@ CONFIGS = {
                         "block 16", B=128, ctx=("fixed", 32768), Hq=64, Hkv=8, kv="fp8_e4m3"),
     "c4": dict(workload="C4: Qwen3-235B-A22B shape (Hq=64, Hkv=4, d=128), B=64, ctx 131072, INT8 KV, "
                         "block 16, split-KV", B=64, ctx=("fixed", 131072), Hq=64, Hkv=4, kv="int8"),
+    "c5": dict(workload="C5: Llama-3-8B shape (Hq=32, Hkv=8, d=128); per step 4 chunked-prefill appends "
+                        "of 2048 tokens + 252 decode sequences in prefix groups of 8 sharing a 1024-token "
+                        "(64-block) prefix, private suffix ~U{64..3072}; block 16", B=252, Hq=32, Hkv=8,
+               kv="int8", prefill_seqs=4, chunk=2048, group=8, prefix=1024, suffix=(64, 3072)),
 }
 METRIC = "quantized paged decode-attn tokens/s and HBM GB/s (% of ~8 TB/s) at 1/2/4/8 B200"
 FALLBACK_HBM_GBS = 6650.0
@@ -425,6 +429,153 @@ def run_ours(args, cfg):
         dist.destroy_process_group()
 
 
+# ---------------------------------------------------------------------------
+# C5: chunked-prefill append + decode mix with prefix-shared blocks
+# ---------------------------------------------------------------------------
+def run_c5(args, cfg):
+    """One step = K1 over 4 x 2048 prefill tokens + 252 decode tokens, then K2
+    over the 252 decode sequences, whose block tables share each group's
+    64-block prefix (BlockAllocator.fork).  Reports decode tokens/s, prefill
+    append GB/s, logical vs DRAM bytes and the quantisation error against
+    fp32 attention over the unquantised K/V (first prefix group)."""
+    import torch
+    from paper_2605_29639_b200 import (BlockAllocator, KVCacheSpec, PagedKVCache,
+                                       paged_decode_attention, quantize_append)
+
+    dev = torch.device("cuda", 0)
+    torch.cuda.set_device(dev)
+    B, Hq, Hkv, G = cfg["B"], cfg["Hq"], cfg["Hkv"], cfg["group"]
+    rng = np.random.default_rng(5)
+    suffix = rng.integers(cfg["suffix"][0], cfg["suffix"][1] + 1, size=B)
+    ngroups = -(-B // G)
+    spec = KVCacheSpec(Hkv, kv_dtype=cfg["kv"])
+    need = ngroups * cfg["prefix"] // 16 + int(np.ceil((suffix + 1) / 16).sum()) + B \
+        + cfg["prefill_seqs"] * cfg["chunk"] // 16 + 64
+    alloc = BlockAllocator(need, bytes_per_block=spec.bytes_per_block)
+    cache = PagedKVCache(spec, need, device=dev)
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(99)
+
+    def kv_rows(n):
+        x = torch.randn((2, n, Hkv, 128), device=dev, generator=gen)
+        return (x * torch.exp(0.5 * torch.randn((2, n, Hkv, 1), device=dev, generator=gen))).to(torch.bfloat16)
+
+    keep = {}  # bf16 K/V of group 0 for the error report: seq -> (k, v)
+    seqs = []
+    for gi in range(ngroups):
+        pid = ("prefix", gi)
+        alloc.allocate(pid)
+        sl = alloc.append_slots(pid, cfg["prefix"])
+        kv = kv_rows(cfg["prefix"])
+        quantize_append(cache, kv[0], kv[1], torch.tensor(sl, dtype=torch.int32, device=dev))
+        for j in range(G):
+            b = gi * G + j
+            if b >= B:
+                break
+            alloc.fork(pid, b)  # prefix is block aligned: shares all 64 blocks, copies nothing
+            sl2 = alloc.append_slots(b, int(suffix[b]))
+            kv2 = kv_rows(int(suffix[b]))
+            quantize_append(cache, kv2[0], kv2[1], torch.tensor(sl2, dtype=torch.int32, device=dev))
+            if gi == 0:
+                keep[b] = (torch.cat([kv[0], kv2[0]]), torch.cat([kv[1], kv2[1]]))
+            seqs.append(b)
+        alloc.free(pid)  # children keep the prefix blocks referenced
+    # decode token slot (stationary: position ctx_b re-written every step)
+    dec_slots = []
+    for b in seqs:
+        dec_slots.append(alloc.append_slots(b, 1)[0])
+    ctx = alloc.seq_lens(seqs)                      # includes the decode token
+    table = torch.from_numpy(alloc.block_table(seqs)).to(dev)
+    lens_d = torch.from_numpy(ctx).to(dev)
+    # prefill chunks: 4 sequences, stationary 2048-token chunk each
+    pf_slots = []
+    for i in range(cfg["prefill_seqs"]):
+        alloc.allocate(("prefill", i))
+        pf_slots += alloc.append_slots(("prefill", i), cfg["chunk"])
+    alloc.check_invariants()
+    T = len(pf_slots) + B
+    kv_step = kv_rows(T)
+    slots_step = torch.tensor(pf_slots + dec_slots, dtype=torch.int32, device=dev)
+    q = torch.randn((B, Hq, 128), device=dev, generator=gen).to(torch.bfloat16)
+    total_pages = int(np.ceil(ctx / 16).sum())
+    from paper_2605_29639_b200 import ops
+    pps = ops.pages_per_split(B, Hkv, total_pages, table.shape[1])
+    ws = torch.zeros(ops.workspace_bytes(B, Hq, Hkv, -(-table.shape[1] // pps)), dtype=torch.uint8, device=dev)
+    out = torch.empty((B, Hq, 128), dtype=torch.bfloat16, device=dev)
+    dec_k = kv_step[0][len(pf_slots):]
+    dec_v = kv_step[1][len(pf_slots):]
+
+    def k1():
+        quantize_append(cache, kv_step[0], kv_step[1], slots_step)
+
+    def k2():
+        paged_decode_attention(q, cache, table, lens_d, out=out, pages_per_split=pps, workspace=ws)
+
+    k1(); k2(); torch.cuda.synchronize()
+    graphs = []
+    for fn in (k1, k2):
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            fn()
+        graphs.append(g)
+    for _ in range(args.warmup):
+        graphs[0].replay(); graphs[1].replay()
+    torch.cuda.synchronize()
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
+    sampler = ClockSampler(0)
+    with sampler:
+        t0 = torch.cuda.Event(enable_timing=True); t1 = torch.cuda.Event(enable_timing=True)
+        t0.record()
+        for i in range(args.steps):
+            ev[i][0].record(); graphs[0].replay(); ev[i][1].record(); graphs[1].replay(); ev[i][2].record()
+        t1.record()
+        torch.cuda.synchronize()
+    ms_step = t0.elapsed_time(t1) / args.steps
+    k1_ms = statistics.mean(e[0].elapsed_time(e[1]) for e in ev)
+    k2_ms = statistics.mean(e[1].elapsed_time(e[2]) for e in ev)
+
+    # quantisation error vs fp32 attention over the unquantised K/V (group 0),
+    # with the stationary decode token included
+    k2()
+    torch.cuda.synchronize()
+    errs = []
+    for i, b in enumerate(list(keep)):
+        kk = torch.cat([keep[b][0], dec_k[b:b + 1]]).float()   # [L, Hkv, d]
+        vv = torch.cat([keep[b][1], dec_v[b:b + 1]]).float()
+        qq = q[b].float().view(Hkv, Hq // Hkv, 128)
+        s_ = torch.einsum("hgd,lhd->hgl", qq, kk) / math.sqrt(128)
+        ref = torch.einsum("hgl,lhd->hgd", torch.softmax(s_, -1), vv).reshape(Hq, 128)
+        o = out[b].float()
+        errs.append(((o - ref).abs().max().item(), ((o - ref).abs().max() / ref.abs().max()).item()))
+    attn_logical = int(ctx.sum()) * Hkv * 264 + B * Hq * 512 + total_pages * 4
+    attn_unique = (ngroups * cfg["prefix"] + int((ctx - cfg["prefix"]).sum())) * Hkv * 264
+    append_bytes = T * Hkv * (2 * 128 * 2 + 2 * 128 + 8) + 4 * T
+    peak, peak_kind = measured_peak()
+    achieved = attn_logical / (k2_ms * 1e-3) / 1e9
+    line = {
+        "metric": METRIC, "value": B / (ms_step * 1e-3), "unit": "tokens/s", "n_gpus": 1,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": cfg["kv"].replace("fp8_e4m3", "e4m3"),
+        "data": "synthetic",
+        "config": {"workload": cfg["workload"], "name": "c5", "decode_seqs": B, "sum_ctx": int(ctx.sum()),
+                   "prefill_tokens_per_step": len(pf_slots), "prefix_groups": ngroups,
+                   "l2": "pool %.2f GB; shared prefixes are re-read by 8 sequences (L2 hits expected)"
+                         % (cache.nbytes() / 1e9)},
+        "k1_ms": k1_ms, "k2_ms": k2_ms,
+        "append_gbs": append_bytes / (k1_ms * 1e-3) / 1e9,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": None, "kernel": "kvq::decode_kernel",
+                     "algorithmic_bytes_per_launch": attn_logical, "unique_kv_bytes": attn_unique,
+                     "avg_launch_ms": k2_ms, "peak_source": peak_kind,
+                     "note": "logical (per-sequence) bytes; prefix pages are shared, so DRAM bytes are lower"},
+        "quant_error_vs_fp32_unquantized": {"max_abs": max(e[0] for e in errs),
+                                            "max_rel_to_row_max": max(e[1] for e in errs),
+                                            "sequences": len(errs)},
+        "gpu_launches": 2 * args.steps, "clocks": sampler.summary(),
+    }
+    print(json.dumps(line), flush=True)
+
+
 def main(argv=None):
     ap = argparse.ArgumentParser(description=__doc__.split("\n\n")[0])
     ap.add_argument("--gpus", type=int, default=1)
@@ -434,11 +585,20 @@ def main(argv=None):
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--kv", default=None, choices=["int8", "fp8_e4m3"],
+                    help="override the config's KV dtype (the C5 INT8 vs FP8 sweep)")
     args = ap.parse_args(argv)
     if args.warmup < 3:
         raise SystemExit("--warmup must be >= 3")
-    cfg = CONFIGS[args.config]
-    if args.impl == "reference":
+    cfg = dict(CONFIGS[args.config])
+    if args.kv:
+        cfg["kv"] = args.kv
+        cfg["workload"] = cfg["workload"].replace("INT8", args.kv.upper()) + f" [{args.kv} KV]"
+    if args.config == "c5":
+        if args.impl == "reference":
+            raise SystemExit("--impl reference is defined on the headline config (c2)")
+        run_c5(args, cfg)
+    elif args.impl == "reference":
         run_reference(args, cfg)
     else:
         run_ours(args, cfg)

@@ -47,27 +47,17 @@ __host__ __device__ __forceinline__ int v_code_off(int tok, int d) {
 }
 
 // ---------------------------------------------------------------------------
-// K1: quantize-on-append.  One warp per (token, kv head, K|V) row of 128.
+// K1: quantize-on-append.  CTA = 16 consecutive tokens x one kv head; warp w
+// quantizes tokens 2w, 2w+1 (K and V rows: 4 rows, loads issued first).
+// When the 16 tokens fill one whole page (slots blk*16 + 0..15, the chunked-
+// prefill case) the page image is assembled in shared memory and written
+// with coalesced 16-byte stores; otherwise each row is scattered directly
+// (decode: one token per sequence).
 // ---------------------------------------------------------------------------
+constexpr int K1_WARPS = 8;
+
 template <int KVD>
-__global__ void __launch_bounds__(256) quant_append_kernel(
-    const __nv_bfloat16* __restrict__ k, const __nv_bfloat16* __restrict__ v, int64_t k_stride,
-    int64_t v_stride, const int32_t* __restrict__ slots, int T, int Hkv,
-    uint8_t* __restrict__ pool, int64_t num_blocks) {
-  const int64_t row = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
-  const int lane = threadIdx.x & 31;
-  if (row >= (int64_t)T * Hkv * 2) return;
-  const int kv = (int)(row & 1);
-  const int64_t th = row >> 1;
-  const int t = (int)(th / Hkv), h = (int)(th % Hkv);
-  const int slot = __ldg(slots + t);
-  if (slot < 0) return;
-  const int64_t blk = slot >> 4;
-  const int tok = slot & 15;
-  if (blk >= num_blocks) return;
-  const __nv_bfloat16* src =
-      (kv ? v + (int64_t)t * v_stride : k + (int64_t)t * k_stride) + h * HD + lane * 4;
-  const uint2 raw = __ldg(reinterpret_cast<const uint2*>(src));
+__device__ __forceinline__ uint32_t quantize4(const uint2 raw, float& scale_out) {
   float x[4];
   x[0] = __uint_as_float(raw.x << 16);
   x[1] = __uint_as_float(raw.x & 0xffff0000u);
@@ -78,11 +68,11 @@ __global__ void __launch_bounds__(256) quant_append_kernel(
   for (int o = 16; o > 0; o >>= 1) a = fmaxf(a, __shfl_xor_sync(FULL, a, o));
   const float qmax = KVD == KVQ_FP8_E4M3 ? 448.0f : 127.0f;
   // Contract: IEEE divisions, one RN multiply, no contraction.
-  const float scale = __fdiv_rn(a, qmax);
+  scale_out = __fdiv_rn(a, qmax);
   const float inv = a > 0.0f ? __fdiv_rn(qmax, a) : 0.0f;
   float y[4];
 #pragma unroll
-  for (int i = 0; i < 4; ++i) y[i] = __fmul_rn(x[i], inv);
+  for (int e = 0; e < 4; ++e) y[e] = __fmul_rn(x[e], inv);
   uint32_t word;
   if constexpr (KVD == KVQ_FP8_E4M3) {
     uint16_t lo, hi;
@@ -92,20 +82,66 @@ __global__ void __launch_bounds__(256) quant_append_kernel(
   } else {
     word = 0;
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      int c = __float2int_rn(y[i]);  // cvt.rni.s32.f32: NaN -> 0, saturating
+    for (int e = 0; e < 4; ++e) {
+      int c = __float2int_rn(y[e]);  // cvt.rni.s32.f32: NaN -> 0, saturating
       c = max(-127, min(127, c));
-      word |= ((uint32_t)(c & 0xff)) << (8 * i);
+      word |= ((uint32_t)(c & 0xff)) << (8 * e);
     }
   }
-  uint8_t* page = pool + ((int64_t)blk * Hkv + h) * PAGE;
-  if (kv == 0) {
-    *reinterpret_cast<uint32_t*>(page + k_code_off(tok, lane * 4)) = word;
-  } else {
+  return word;
+}
+
+template <int KVD>
+__global__ void __launch_bounds__(32 * K1_WARPS) quant_append_kernel(
+    const __nv_bfloat16* __restrict__ k, const __nv_bfloat16* __restrict__ v, int64_t k_stride,
+    int64_t v_stride, const int32_t* __restrict__ slots, int T, int Hkv,
+    uint8_t* __restrict__ pool, int64_t num_blocks) {
+  __shared__ __align__(16) uint8_t img[PAGE];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int t0 = blockIdx.x * 16, h = blockIdx.y;
+  // Whole-page test: 16 in-range tokens with slots blk*16 + 0..15.
+  int my_slot = -1;
+  if (threadIdx.x < 16 && t0 + threadIdx.x < T) my_slot = __ldg(slots + t0 + threadIdx.x);
+  const int first = t0 < T ? __ldg(slots + t0) : -1;
+  const bool mine_ok = threadIdx.x >= 16 ||
+                       (my_slot >= 0 && my_slot == first + (int)threadIdx.x && (first & 15) == 0 &&
+                        (first >> 4) < num_blocks);
+  const bool whole = __syncthreads_and(mine_ok);
+
+  uint2 raw[4];
+  int slot[2];
 #pragma unroll
-    for (int i = 0; i < 4; ++i) page[v_code_off(tok, lane * 4 + i)] = (uint8_t)(word >> (8 * i));
+  for (int i = 0; i < 2; ++i) {
+    const int t = t0 + 2 * warp + i;
+    slot[i] = t < T ? __ldg(slots + t) : -1;
+    const bool live = slot[i] >= 0 && (slot[i] >> 4) < num_blocks;
+    raw[2 * i] = live ? __ldg(reinterpret_cast<const uint2*>(k + (int64_t)t * k_stride + h * HD + lane * 4))
+                      : make_uint2(0, 0);
+    raw[2 * i + 1] = live ? __ldg(reinterpret_cast<const uint2*>(v + (int64_t)t * v_stride + h * HD + lane * 4))
+                          : make_uint2(0, 0);
   }
-  if (lane == 0) *reinterpret_cast<float*>(page + (kv ? VS_OFF : KS_OFF) + 4 * tok) = scale;
+#pragma unroll
+  for (int r4 = 0; r4 < 4; ++r4) {
+    const int i = r4 >> 1, kv = r4 & 1;
+    if (slot[i] < 0 || (slot[i] >> 4) >= num_blocks) continue;  // warp-uniform
+    const int tok = slot[i] & 15;
+    float scale;
+    const uint32_t word = quantize4<KVD>(raw[r4], scale);
+    uint8_t* page = whole ? img : pool + ((int64_t)(slot[i] >> 4) * Hkv + h) * PAGE;
+    if (kv == 0) {
+      *reinterpret_cast<uint32_t*>(page + k_code_off(tok, lane * 4)) = word;
+    } else {
+#pragma unroll
+      for (int e = 0; e < 4; ++e) page[v_code_off(tok, lane * 4 + e)] = (uint8_t)(word >> (8 * e));
+    }
+    if (lane == 0) *reinterpret_cast<float*>(page + (kv ? VS_OFF : KS_OFF) + 4 * tok) = scale;
+  }
+  if (whole) {
+    __syncthreads();
+    uint4* dst = reinterpret_cast<uint4*>(pool + ((int64_t)(first >> 4) * Hkv + h) * PAGE);
+    const uint4* src = reinterpret_cast<const uint4*>(img);
+    for (int i = threadIdx.x; i < PAGE / 16; i += 32 * K1_WARPS) dst[i] = src[i];
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -496,11 +532,17 @@ __global__ void __launch_bounds__(THREADS, Geo<HI>::CTAS) decode_kernel(const De
     float vs_r = lds32f(pg + VS_OFF + 4 * r), vs_r8 = lds32f(pg + VS_OFF + 32 + 4 * r);
 
     // ---- S^T = K . Q^T : two accumulator chains per n-tile (k-steps 0-3, 4-7)
+    // The INT8 K bias (kbias) seeds the accumulator, so no separate subtraction.
+    // g <= 8: two chains (k-steps 0-3 / 4-7) for ILP; g > 8: the two n-tiles interleave.
+    constexpr bool TWO_CHAINS = !HI;
     float sa[NT][4], sb[NT][4];
 #pragma unroll
-    for (int nt = 0; nt < NT; ++nt)
+    for (int nt = 0; nt < NT; ++nt) {
+      sa[nt][0] = sa[nt][2] = -kbias[nt][0];
+      sa[nt][1] = sa[nt][3] = -kbias[nt][1];
 #pragma unroll
-      for (int e = 0; e < 4; ++e) sa[nt][e] = sb[nt][e] = 0.0f;
+      for (int e = 0; e < 4; ++e) sb[nt][e] = 0.0f;
+    }
     {
       const uint32_t kr[8] = {k0.x, k0.y, k0.z, k0.w, k1.x, k1.y, k1.z, k1.w};
       const uint32_t kr8[8] = {k2.x, k2.y, k2.z, k2.w, k3.x, k3.y, k3.z, k3.w};
@@ -511,7 +553,7 @@ __global__ void __launch_bounds__(THREADS, Geo<HI>::CTAS) decode_kernel(const De
         codes_to_f16x2<KVD, true>(kr8[i], a1, a3);
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt)
-          mma16816(i < 4 ? sa[nt] : sb[nt], a0, a1, a2, a3, qf[nt][i][0], qf[nt][i][1]);
+          mma16816((TWO_CHAINS && i >= 4) ? sb[nt] : sa[nt], a0, a1, a2, a3, qf[nt][i][0], qf[nt][i][1]);
       }
     }
     // ---- scores in log2 units; thread holds tokens r, r+8 x heads 2c, 2c+1 per n-tile
@@ -525,10 +567,14 @@ __global__ void __launch_bounds__(THREADS, Geo<HI>::CTAS) decode_kernel(const De
     float mx[NT][2];
 #pragma unroll
     for (int nt = 0; nt < NT; ++nt) {
-      sc[nt][0] = ok_r ? (sa[nt][0] + sb[nt][0] - kbias[nt][0]) * kq_r : -INFINITY;
-      sc[nt][1] = ok_r ? (sa[nt][1] + sb[nt][1] - kbias[nt][1]) * kq_r : -INFINITY;
-      sc[nt][2] = ok_r8 ? (sa[nt][2] + sb[nt][2] - kbias[nt][0]) * kq_r8 : -INFINITY;
-      sc[nt][3] = ok_r8 ? (sa[nt][3] + sb[nt][3] - kbias[nt][1]) * kq_r8 : -INFINITY;
+      const float s0 = TWO_CHAINS ? sa[nt][0] + sb[nt][0] : sa[nt][0];
+      const float s1 = TWO_CHAINS ? sa[nt][1] + sb[nt][1] : sa[nt][1];
+      const float s2 = TWO_CHAINS ? sa[nt][2] + sb[nt][2] : sa[nt][2];
+      const float s3 = TWO_CHAINS ? sa[nt][3] + sb[nt][3] : sa[nt][3];
+      sc[nt][0] = ok_r ? s0 * kq_r : -INFINITY;
+      sc[nt][1] = ok_r ? s1 * kq_r : -INFINITY;
+      sc[nt][2] = ok_r8 ? s2 * kq_r8 : -INFINITY;
+      sc[nt][3] = ok_r8 ? s3 * kq_r8 : -INFINITY;
       mx[nt][0] = fmaxf(sc[nt][0], sc[nt][2]);
       mx[nt][1] = fmaxf(sc[nt][1], sc[nt][3]);
     }
@@ -712,17 +758,20 @@ __global__ void __launch_bounds__(THREADS, Geo<HI>::CTAS) decode_kernel(const De
   if (nsplit == 1) return;
 
   // ===== fused split-KV combine: the last CTA of (b, h) merges all splits =====
-  __threadfence();
+  // bar.sync orders the CTA's partial stores before thread 0's acq_rel atomic
+  // (release at gpu scope, cumulative); the last arriver's acquire + bar.sync
+  // make every split's partials visible to its threads.
   __syncthreads();
   if (tid == 0) {
-    const int prev = atomicAdd(p.counters + (int64_t)b * p.Hkv + h, 1);
+    int* ctr = p.counters + (int64_t)b * p.Hkv + h;
+    int prev;
+    asm volatile("atom.add.acq_rel.gpu.s32 %0, [%1], 1;" : "=r"(prev) : "l"(ctr) : "memory");
     const int last = prev == nsplit - 1;
-    if (last) p.counters[(int64_t)b * p.Hkv + h] = 0;  // reset for the next launch / replay
+    if (last) asm volatile("st.relaxed.gpu.s32 [%0], 0;" ::"l"(ctr) : "memory");  // reset for replay
     *flag = last;
   }
   __syncthreads();
   if (!*flag) return;
-  __threadfence();
   for (int item = tid; item < nrow_items; item += THREADS) {
     const int row = item / (HD / 8), d0 = (item % (HD / 8)) * 8;
     const int head = h * g + row;
@@ -814,15 +863,15 @@ int kvq_quant_append(const void* k, const void* v, int64_t k_token_stride, int64
   if (kv_dtype != KVQ_INT8 && kv_dtype != KVQ_FP8_E4M3)
     return fail(KVQ_EUNSUPPORTED, "quant_append: unknown kv dtype");
   if (int rc = check_device()) return rc;
-  const int64_t rows = (int64_t)T * Hkv * 2;
-  const dim3 grid((unsigned)((rows + 7) / 8));
+  if (Hkv > 65535) return fail(KVQ_EINVAL, "quant_append: Hkv too large");
+  const dim3 grid((unsigned)((T + 15) / 16), (unsigned)Hkv);
   auto st = static_cast<cudaStream_t>(stream);
   if (kv_dtype == KVQ_INT8)
-    kvq::quant_append_kernel<KVQ_INT8><<<grid, 256, 0, st>>>(
+    kvq::quant_append_kernel<KVQ_INT8><<<grid, 32 * kvq::K1_WARPS, 0, st>>>(
         static_cast<const __nv_bfloat16*>(k), static_cast<const __nv_bfloat16*>(v), k_token_stride,
         v_token_stride, slot_mapping, T, Hkv, static_cast<uint8_t*>(pool), num_blocks);
   else
-    kvq::quant_append_kernel<KVQ_FP8_E4M3><<<grid, 256, 0, st>>>(
+    kvq::quant_append_kernel<KVQ_FP8_E4M3><<<grid, 32 * kvq::K1_WARPS, 0, st>>>(
         static_cast<const __nv_bfloat16*>(k), static_cast<const __nv_bfloat16*>(v), k_token_stride,
         v_token_stride, slot_mapping, T, Hkv, static_cast<uint8_t*>(pool), num_blocks);
   return check_launch("quant_append");

@@ -82,3 +82,21 @@ def test_append_strided_and_skipped(cuda):
     O.quant_append(bf16_bits(k.contiguous()), bf16_bits(v.contiguous()), slots, O.INT8, ref)
     assert np.array_equal(cache.pool.cpu().numpy(), ref)
     assert not ref[0].any(), "block 0 must stay untouched"
+
+
+@pytest.mark.parametrize("kv_dtype", ["int8", "fp8_e4m3"])
+def test_append_whole_pages_and_mixed(cuda, kv_dtype):
+    """Chunked-prefill shape: runs of 16 block-aligned slots take the
+    whole-page path; a misaligned run and scattered decode slots in the same
+    call take the per-row path.  Bytes must match the oracle either way."""
+    Hkv = 8
+    num_blocks = 40
+    slots = list(range(5 * 16, 9 * 16))            # 4 whole pages (blocks 5..8)
+    slots += list(range(12 * 16 + 3, 14 * 16 + 3))  # 32 slots, not block-aligned
+    slots += [30 * 16 + 7, 2 * 16 + 0, 33 * 16 + 15, -1, 20 * 16 + 1]
+    slots += list(range(36 * 16, 36 * 16 + 13))      # partial page
+    slots = np.asarray(slots, dtype=np.int32)
+    T = len(slots)
+    k, v = make_kv(T, Hkv, 31, kind="k"), make_kv(T, Hkv, 32, kind="v")
+    gpu, ref = run_both(k, v, slots, Hkv, kv_dtype, num_blocks, cuda)
+    assert np.array_equal(gpu, ref), f"{(gpu != ref).sum()} bytes differ"

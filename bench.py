@@ -242,60 +242,65 @@ def run_ours(args, cfg):
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
 
-    from paper_2605_29639_b200 import KVCacheSpec, PagedKVCache, paged_decode_attention, quantize_append
-    from paper_2605_29639_b200.shard import head_partition
+    from paper_2605_29639_b200 import KVCacheSpec, PagedKVCache, quantize_append
+    from paper_2605_29639_b200.session import DecodeSession
+    from paper_2605_29639_b200.shard import OutputGather, plan_shards
 
     B, Hq, Hkv = cfg["B"], cfg["Hq"], cfg["Hkv"]
-    (kv0, kv1), (q0, q1) = head_partition(Hq, Hkv, world, rank)
+    lens_all = ctx_lens(cfg)
+    # KV-head split when Hkv % N == 0, else KV-head groups x LPT batch parts (C4 at N = 8)
+    plan = plan_shards(Hq, Hkv, world, rank, lens_all + 1)
+    (kv0, kv1), (q0, q1) = plan.kv_range, plan.q_range
     Hkv_loc, Hq_loc = kv1 - kv0, q1 - q0
-    lens = ctx_lens(cfg)
+    seqs = plan.seqs
+    lens = lens_all[seqs]
+    B_loc = len(seqs)
     L1 = lens + 1
     nblk = np.ceil(L1 / 16).astype(np.int64)
     max_blocks = int(nblk.max())
     num_blocks = int(nblk.sum())
-    rng = np.random.default_rng(7)
+    rng = np.random.default_rng(7 + rank)
     perm = rng.permutation(num_blocks).astype(np.int32)
-    table = np.zeros((B, max_blocks), dtype=np.int32)
+    table = np.zeros((B_loc, max_blocks), dtype=np.int32)
     pos = 0
-    for b in range(B):
+    for b in range(B_loc):
         table[b, : nblk[b]] = perm[pos: pos + nblk[b]]
         pos += nblk[b]
     spec = KVCacheSpec(Hkv_loc, kv_dtype=cfg["kv"])
     cache = PagedKVCache(spec, num_blocks, device=dev)
     table_d = torch.from_numpy(table).to(dev)
 
-    # Fill the cache through K1 (the product path), in chunks, same data on every
-    # rank for its own heads (seeded by global head index).
+    # Fill this rank's pool (its KV heads, its sequences) through K1, in chunks.
     gen = torch.Generator(device=dev)
-    gen.manual_seed(1234)
-    tok_b = np.repeat(np.arange(B), lens)
-    tok_t = np.concatenate([np.arange(L) for L in lens]) if B else np.zeros(0, np.int64)
+    gen.manual_seed(1234 + rank)
+    tok_b = np.repeat(np.arange(B_loc), lens)
+    tok_t = np.concatenate([np.arange(L) for L in lens]) if B_loc else np.zeros(0, np.int64)
     all_slots = (table[tok_b, tok_t // 16].astype(np.int64) * 16 + tok_t % 16).astype(np.int32)
     chunk = 1 << 15
     for s0 in range(0, len(all_slots), chunk):
         sl = torch.from_numpy(all_slots[s0: s0 + chunk]).to(dev)
         n = sl.numel()
-        kv = torch.randn((2, n, Hkv, 128), device=dev, generator=gen)
-        kv = kv * torch.exp(0.5 * torch.randn((2, n, Hkv, 1), device=dev, generator=gen))
-        kv = kv[:, :, kv0:kv1].to(torch.bfloat16)
+        kv = torch.randn((2, n, Hkv_loc, 128), device=dev, generator=gen)
+        kv = (kv * torch.exp(0.5 * torch.randn((2, n, Hkv_loc, 1), device=dev, generator=gen))).to(torch.bfloat16)
         quantize_append(cache, kv[0], kv[1], sl)
     del kv
     seq_lens_d = torch.from_numpy(L1.astype(np.int32)).to(dev)
-    slots_step = torch.from_numpy((table[np.arange(B), lens // 16].astype(np.int64) * 16 + lens % 16)
+    slots_step = torch.from_numpy((table[np.arange(B_loc), lens // 16].astype(np.int64) * 16 + lens % 16)
                                   .astype(np.int32)).to(dev)
-    q_full = torch.randn((B, Hq, 128), device=dev, generator=gen).to(torch.bfloat16)
-    q = q_full[:, q0:q1].contiguous()
-    k_new = torch.randn((B, Hkv, 128), device=dev, generator=gen).to(torch.bfloat16)[:, kv0:kv1].contiguous()
-    v_new = torch.randn((B, Hkv, 128), device=dev, generator=gen).to(torch.bfloat16)[:, kv0:kv1].contiguous()
+    q = torch.randn((B_loc, Hq_loc, 128), device=dev, generator=gen).to(torch.bfloat16)
+    k_new = torch.randn((B_loc, Hkv_loc, 128), device=dev, generator=gen).to(torch.bfloat16)
+    v_new = torch.randn((B_loc, Hkv_loc, 128), device=dev, generator=gen).to(torch.bfloat16)
     total_pages = int(nblk.sum())
 
-    from paper_2605_29639_b200.session import DecodeSession
-    sess = DecodeSession(cache, table_d, B, Hq_loc, total_pages=total_pages, head_major=True,
-                         gather_group=dist.group.WORLD if world > 1 else None, world=world)
+    def make_gather():
+        return OutputGather(plan, Hq, B, torch.bfloat16, dev)
+
+    sess = DecodeSession(cache, table_d, B_loc, Hq_loc, total_pages=total_pages, head_major=True,
+                         gather_factory=make_gather if world > 1 else None)
     buf = sess.device_buffers(0)
     for name, t in (("q", q), ("k", k_new), ("v", v_new), ("slots", slots_step), ("lens", seq_lens_d)):
         buf[name].copy_(t)
-    out_all = torch.empty((Hq, B, 128), dtype=torch.bfloat16, device=dev) if world > 1 else None
+    gather_dev = make_gather() if world > 1 else None
 
     def barrier():
         if world > 1:
@@ -322,7 +327,7 @@ def run_ours(args, cfg):
         if ev is not None:
             ev[1].record()
         if world > 1:
-            dist.all_gather_into_tensor(out_all, buf["out"])
+            gather_dev(buf["out"])
 
     for _ in range(args.warmup):
         step()
@@ -386,7 +391,7 @@ def run_ours(args, cfg):
         if world > 1:
             dist.destroy_process_group()
         return
-    attn_bytes, append_bytes = algorithmic_bytes(lens, Hq_loc, Hkv_loc, B)
+    attn_bytes, append_bytes = algorithmic_bytes(lens, Hq_loc, Hkv_loc, B_loc)
     peak, peak_kind = measured_peak()
     achieved = attn_bytes / (k2_ms * 1e-3) / 1e9
     traffic = None
@@ -403,7 +408,10 @@ def run_ours(args, cfg):
         "scaling": "strong" if world > 1 else "weak", "vs_baseline": None,
         "dtype": cfg["kv"].replace("fp8_e4m3", "e4m3"), "data": "synthetic",
         "config": {"workload": cfg["workload"], "name": args.config, "global_batch": B,
-                   "sum_ctx": int(L1.sum()), "parallelism": f"kv-head tp{world}" if world > 1 else "1 GPU",
+                   "sum_ctx": int((lens_all + 1).sum()),
+                   "parallelism": (f"kv-head tp{world}" if plan.b_split == 1 else
+                                   f"{plan.h_split} kv-head groups x {plan.b_split} LPT batch parts")
+                   if world > 1 else "1 GPU",
                    "l2": "inputs larger than L2 (pool %.2f GB vs 126 MB L2); no flush" % (cache.nbytes() * world / 1e9)
                    if cache.nbytes() * world > 4 * 126e6 else "pool fits in L2: L2-resident numbers",
                    "step": "K1 append of B rows + K2 paged decode attention (+ all-gather if N>1); "

@@ -33,13 +33,15 @@ class DecodeSession:
     def __init__(self, cache: PagedKVCache, block_table: torch.Tensor, batch: int, num_q_heads: int,
                  *, total_pages: Optional[int] = None, out_dtype: torch.dtype = torch.bfloat16,
                  head_major: bool = False, sm_scale: Optional[float] = None, depth: int = 2,
-                 gather_group=None, world: int = 1):
-        """With ``gather_group`` (KV-head sharding, paper_2605_29639_b200.shard)
-        the local head-major output ``[Hq/P, B, d]`` is all-gathered into
-        ``[Hq, B, d]`` on the compute stream before the download."""
+                 gather_factory=None):
+        """With ``gather_factory`` (returning a
+        :class:`paper_2605_29639_b200.shard.OutputGather`, one per buffer slot,
+        for KV-head / 2-D sharding) the local head-major output
+        ``[Hq_loc, B_r, d]`` is assembled into ``[Hq, B, d]`` on the compute
+        stream before the download."""
         dev = cache.device
-        self.gather_group, self.world = gather_group, world
-        if gather_group is not None:
+        self.sharded = gather_factory is not None
+        if self.sharded:
             head_major = True
         self.cache, self.block_table = cache, block_table
         self.B, self.Hq, self.Hkv = batch, num_q_heads, cache.spec.num_kv_heads
@@ -63,12 +65,10 @@ class DecodeSession:
                 slots=torch.empty((batch,), dtype=torch.int32, device=dev),
                 lens=torch.empty((batch,), dtype=torch.int32, device=dev),
                 out=torch.empty(oshape, dtype=out_dtype, device=dev),
-                out_all=(torch.empty((num_q_heads * world, batch, 128), dtype=out_dtype, device=dev)
-                         if gather_group is not None else None),
                 ws=torch.zeros(workspace_bytes(batch, num_q_heads, self.Hkv, max_splits),
                                dtype=torch.uint8, device=dev),
                 in_ready=torch.cuda.Event(), done=torch.cuda.Event(), out_done=torch.cuda.Event(),
-                used=False))
+                gather=gather_factory() if self.sharded else None, used=False))
         self.step_idx = 0
 
     def _kernels(self, buf) -> None:
@@ -98,13 +98,11 @@ class DecodeSession:
             self.compute.wait_event(buf["out_done"])   # previous download of this out buffer
         with torch.cuda.stream(self.compute):
             self._kernels(buf)
-            if self.gather_group is not None:
-                import torch.distributed as dist
-                dist.all_gather_into_tensor(buf["out_all"], buf["out"], group=self.gather_group)
+            full = buf["gather"](buf["out"]) if self.sharded else buf["out"]
         buf["done"].record(self.compute)
         with torch.cuda.stream(self.d2h):
             self.d2h.wait_event(buf["done"])
-            out_h.copy_(buf["out_all"] if self.gather_group is not None else buf["out"], non_blocking=True)
+            out_h.copy_(full, non_blocking=True)
             buf["out_done"].record(self.d2h)
         buf["used"] = True
         return buf["out_done"]

@@ -14,8 +14,11 @@ op.  With P == 1 there is no collective at all.
 """
 from __future__ import annotations
 
-from typing import Callable, Optional, Tuple
+import math
+from dataclasses import dataclass
+from typing import Callable, List, Optional, Sequence, Tuple
 
+import numpy as np
 import torch
 import torch.distributed as dist
 
@@ -32,6 +35,74 @@ def head_partition(num_q_heads: int, num_kv_heads: int, world: int, rank: int
     kv = num_kv_heads // world
     g = num_q_heads // num_kv_heads
     return (rank * kv, (rank + 1) * kv), (rank * kv * g, (rank + 1) * kv * g)
+
+
+def lpt_assign(lengths: Sequence[int], bins: int) -> List[List[int]]:
+    """Longest-processing-time greedy balance of sequences (by context length,
+    i.e. KV bytes) over ``bins``: longest first, each to the least-loaded bin,
+    ties to the lowest bin -- the reference's file balancer
+    (``load_planner.py:145-157``) applied to KV tokens.  Bins come back sorted."""
+    loads = [0] * bins
+    out: List[List[int]] = [[] for _ in range(bins)]
+    for i in sorted(range(len(lengths)), key=lambda i: (-int(lengths[i]), i)):
+        j = min(range(bins), key=lambda j: (loads[j], j))
+        loads[j] += int(lengths[i])
+        out[j].append(i)
+    return [sorted(x) for x in out]
+
+
+@dataclass
+class ShardPlan:
+    """2-D (KV head group x batch part) partition for one rank.
+
+    ``h_split = gcd(Hkv, P)`` head groups x ``b_split = P / h_split`` batch
+    parts; rank = head_group * b_split + batch_part.  With Hkv % P == 0 this is
+    the plain KV-head split (b_split = 1).  C4 (Hkv = 4, P = 8) gets 4 head
+    groups x 2 token-balanced batch halves, so no GPU idles and no extra
+    exchange is needed beyond the one all-gather."""
+    world: int
+    rank: int
+    h_split: int
+    b_split: int
+    kv_range: Tuple[int, int]
+    q_range: Tuple[int, int]
+    seqs: np.ndarray                 # global sequence ids this rank attends (sorted)
+    parts: List[List[int]]           # sequences of every batch part
+    b_max: int                       # padded per-rank batch for the all-gather
+
+    @property
+    def num_q_local(self) -> int:
+        return self.q_range[1] - self.q_range[0]
+
+    def gather_index(self, num_q_heads: int, batch: int) -> np.ndarray:
+        """Flat row index into the gathered ``[P, Hq_loc, b_max]`` buffer for
+        every output row ``(h, b)`` of ``[Hq, B]``."""
+        hq_loc = num_q_heads // self.h_split
+        idx = np.zeros((num_q_heads, batch), dtype=np.int64)
+        for hg in range(self.h_split):
+            for bs, seqs in enumerate(self.parts):
+                rk = hg * self.b_split + bs
+                for pos, b in enumerate(seqs):
+                    for hl in range(hq_loc):
+                        idx[hg * hq_loc + hl, b] = (rk * hq_loc + hl) * self.b_max + pos
+        return idx.reshape(-1)
+
+
+def plan_shards(num_q_heads: int, num_kv_heads: int, world: int, rank: int,
+                seq_lens: Sequence[int]) -> ShardPlan:
+    if num_q_heads % num_kv_heads:
+        raise ValueError("num_q_heads must be a multiple of num_kv_heads")
+    h_split = math.gcd(num_kv_heads, world)
+    b_split = world // h_split
+    if len(seq_lens) < b_split:
+        raise ValueError("fewer sequences than batch parts")
+    hg, bs = divmod(rank, b_split)
+    kv = num_kv_heads // h_split
+    g = num_q_heads // num_kv_heads
+    parts = lpt_assign(seq_lens, b_split)
+    return ShardPlan(world, rank, h_split, b_split, (hg * kv, (hg + 1) * kv),
+                     (hg * kv * g, (hg + 1) * kv * g), np.asarray(parts[bs], dtype=np.int64),
+                     parts, max(len(x) for x in parts))
 
 
 class ShardedDecodeAttention:
@@ -75,6 +146,66 @@ class ShardedDecodeAttention:
                               device=o_loc.device)
         dist.all_gather_into_tensor(out, o_loc.contiguous(), group=self.group)
         return out
+
+
+class OutputGather:
+    """Assembles ``[Hq, B, d]`` from every rank's head-major ``[Hq_loc, B_r, d]``:
+    one all-gather of equal-size padded pieces, then (only when the batch is
+    split) one row gather.  Buffers are preallocated, so the call is stream-
+    ordered and can run inside a serving loop without allocation."""
+
+    def __init__(self, plan: "ShardPlan", num_q_heads: int, batch: int, dtype, device,
+                 group: Optional[dist.ProcessGroup] = None):
+        self.plan, self.group = plan, group
+        hq_loc = plan.num_q_local
+        self.piece = torch.zeros((hq_loc, plan.b_max, 128), dtype=dtype, device=device)
+        self.gathered = torch.empty((plan.world * hq_loc, plan.b_max, 128), dtype=dtype, device=device)
+        self.simple = plan.b_split == 1   # rank-major concat is already [Hq, B, d]
+        self.idx = (None if self.simple else
+                    torch.as_tensor(plan.gather_index(num_q_heads, batch), device=device))
+        self.out = self.gathered.view(num_q_heads, batch, 128) if self.simple else \
+            torch.empty((num_q_heads, batch, 128), dtype=dtype, device=device)
+
+    def __call__(self, out_local: torch.Tensor) -> torch.Tensor:
+        if self.simple:
+            dist.all_gather_into_tensor(self.gathered, out_local.contiguous(), group=self.group)
+            return self.out
+        self.piece[:, : out_local.shape[1]].copy_(out_local)
+        dist.all_gather_into_tensor(self.gathered, self.piece, group=self.group)
+        torch.index_select(self.gathered.view(-1, 128), 0, self.idx, out=self.out.view(-1, 128))
+        return self.out
+
+
+class Sharded2DDecodeAttention:
+    """Decode attention over a 2-D (KV head group x batch part) partition.
+
+    ``local_attention(q_local[B_r, Hq_loc, d]) -> [Hq_loc, B_r, d]`` attends this
+    rank's sequences over its heads (rows of ``plan.seqs``); :class:`OutputGather`
+    assembles ``[Hq, B, d]``."""
+
+    def __init__(self, num_q_heads: int, num_kv_heads: int, seq_lens: Sequence[int],
+                 group: Optional[dist.ProcessGroup] = None,
+                 local_attention: Optional[Callable[[torch.Tensor], torch.Tensor]] = None):
+        self.group = group
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        self.Hq, self.Hkv, self.B = num_q_heads, num_kv_heads, len(seq_lens)
+        self.plan = plan_shards(num_q_heads, num_kv_heads, self.world, self.rank, seq_lens)
+        self.local_attention = local_attention
+        self._gather = None
+
+    def local_q(self, q: torch.Tensor) -> torch.Tensor:
+        q0, q1 = self.plan.q_range
+        seqs = torch.as_tensor(self.plan.seqs, device=q.device)
+        return q.index_select(0, seqs)[:, q0:q1].contiguous()
+
+    def __call__(self, q: torch.Tensor) -> torch.Tensor:
+        o_loc = self.local_attention(self.local_q(q))          # [Hq_loc, B_r, d]
+        if self.world == 1:
+            return o_loc
+        if self._gather is None:
+            self._gather = OutputGather(self.plan, self.Hq, self.B, o_loc.dtype, o_loc.device, self.group)
+        return self._gather(o_loc)
 
 
 def cuda_local_attention(cache, block_table, seq_lens, **kw) -> Callable[[torch.Tensor], torch.Tensor]:

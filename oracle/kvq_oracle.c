@@ -100,15 +100,20 @@ void kvqo_quantize_rows(const uint16_t* x, int64_t rows, int kv_dtype, uint8_t* 
     quantize_row(x + r * KVQO_HEAD_DIM, kv_dtype, codes + r * KVQO_HEAD_DIM, scales + r);
 }
 
-/* Page layout.  K: 16 rows x 128 B, 16-byte chunk j of row t
- * stored at chunk j ^ ((t & 1) << 2).  V: token pairs interleaved -- pair-row
+/* Page layout.  K: row pair p = t & 7 (tokens p, p+8; 256 B)
+ * of 16-byte units; unit (4j + c) ^ ((p & 1) << 2) holds, as 4-byte words,
+ * K[p][16c+4j..], K[p+8][16c+4j..], K[p][64+16c+4j..], K[p+8][64+16c+4j..].
+ * V: token pairs interleaved -- pair-row
  * p = t/2 holds byte 2d + (t & 1); the 256-byte pair-row is two 128-byte rows
  * R = 2p + (L >= 128) whose chunks are stored at j ^ (R & 7).  Scales: K at
  * 4096 + 4t, V at 4160 + 4t (fp32). */
 int kvqo_code_offset(int kv, int token, int d) {
   if (kv == 0) {
-    const int j = d >> 4;
-    return token * 128 + ((j ^ ((token & 1) << 2)) << 4) + (d & 15);
+    const int p = token & 7, hi_row = token >> 3;
+    const int half = d >> 6, dd = d & 63;
+    const int c = dd >> 4, j = (dd >> 2) & 3;
+    const int unit = (4 * j + c) ^ ((p & 1) << 2);
+    return p * 256 + unit * 16 + (2 * half + hi_row) * 4 + (d & 3);
   }
   const int L = 2 * d + (token & 1);
   const int R = 2 * (token >> 1) + (L >> 7);

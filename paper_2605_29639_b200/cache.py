@@ -116,8 +116,9 @@ def _layout_index() -> Tuple[np.ndarray, np.ndarray]:
     code = np.zeros((2, BLOCK_SIZE, HEAD_DIM), dtype=np.int64)
     for t in range(BLOCK_SIZE):
         for d in range(HEAD_DIM):
-            j = d >> 4
-            code[0, t, d] = t * 128 + ((j ^ ((t & 1) << 2)) << 4) + (d & 15)
+            pr, hi_row, half, dd = t & 7, t >> 3, d >> 6, d & 63
+            unit = (4 * ((dd >> 2) & 3) + (dd >> 4)) ^ ((pr & 1) << 2)
+            code[0, t, d] = pr * 256 + unit * 16 + (2 * half + hi_row) * 4 + (d & 3)
             L = 2 * d + (t & 1)
             R = 2 * (t >> 1) + (L >> 7)
             l = L & 127

@@ -36,8 +36,14 @@ constexpr unsigned FULL = 0xffffffffu;
 // Page layout helpers.
 // ---------------------------------------------------------------------------
 __host__ __device__ __forceinline__ int k_code_off(int tok, int d) {
-  const int j = d >> 4;
-  return tok * 128 + ((j ^ ((tok & 1) << 2)) << 4) + (d & 15);
+  // Row pair p = tok & 7 holds tokens p and p + 8 (256 B).  Its 16-byte unit
+  // (4j + c) ^ ((p & 1) << 2) is one MMA A-fragment quad:
+  //   [K[p][16c+4j..+3], K[p+8][16c+4j..+3], K[p][64+16c+4j..+3], K[p+8][64+16c+4j..+3]]
+  const int p = tok & 7, hi_row = tok >> 3;
+  const int half = d >> 6, dd = d & 63;
+  const int c = dd >> 4, j = (dd >> 2) & 3, e = d & 3;
+  const int unit = (4 * j + c) ^ ((p & 1) << 2);
+  return p * 256 + unit * 16 + (2 * half + hi_row) * 4 + e;
 }
 __host__ __device__ __forceinline__ int v_code_off(int tok, int d) {
   const int L = 2 * d + (tok & 1);
@@ -208,6 +214,17 @@ __device__ __forceinline__ void mma16816(float (&c)[4], uint32_t a0, uint32_t a1
       : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
       : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
 }
+__device__ __forceinline__ void mma16832_s8(int (&c)[4], uint32_t a0, uint32_t a1, uint32_t a2,
+                                            uint32_t a3, uint32_t b0, uint32_t b1) {
+  asm("mma.sync.aligned.m16n8k32.row.col.s32.s8.s8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+      "{%8,%9}, {%0,%1,%2,%3};"
+      : "+r"(c[0]), "+r"(c[1]), "+r"(c[2]), "+r"(c[3])
+      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ uint32_t pack_s8x4(int a, int b, int c, int d) {
+  return (uint32_t)(a & 0xff) | ((uint32_t)(b & 0xff) << 8) | ((uint32_t)(c & 0xff) << 16) |
+         ((uint32_t)d << 24);
+}
 __device__ __forceinline__ uint32_t pack_half2(float lo, float hi) {
   __half2 h = __floats2half2_rn(lo, hi);
   return *reinterpret_cast<uint32_t*>(&h);
@@ -279,7 +296,7 @@ struct Geo {
   static constexpr int CTAS = 4;                  // resident CTAs per SM (regs + smem)
   // g > 8 keeps the Q^T fragments in shared memory (one copy per CTA, read with
   // one conflict-free LDS.64 per k-step) so the live set fits 128 registers.
-  static constexpr size_t QSM = HI ? (size_t)NT * 8 * 32 * 8 : 0;
+  static constexpr size_t QSM = HI ? (size_t)NT * 8 * 32 * 8 : 0;  // [nt][k-step pair][lane] uint4
   static constexpr size_t SMEM = (size_t)NW * S * PAGE + QSM + NW * S * sizeof(uint64_t) + 16;
   static_assert((size_t)NW * S * PAGE >= (size_t)NW * 16 * HD * 4 + 2 * NW * 16 * 4,
                 "merge scratch must fit in the ring");
@@ -447,64 +464,78 @@ __global__ void __launch_bounds__(THREADS, Geo<HI>::CTAS) decode_kernel(const De
       }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) amax = fmaxf(amax, __shfl_xor_sync(FULL, amax, o));
-    // Exact power-of-two prescale so max|q'| < 2^14 (fp16-safe); undone in qscale.
-    int ex = 0;
-    if (amax > 0.0f) frexpf(amax, &ex);
-    const float pre = pow2i(14 - ex);
-    qscale = p.sm_scale_log2 / pre;
+    if constexpr (KVD == KVQ_INT8) {
+      // INT8 K feeds the s8 tensor cores directly (no dequantisation at all):
+      // q = s1 * (q1 + q2 / 128) with int8 q1, q2 (error <= amax / 32512), two
+      // IMMA per k-step, S = s1 * (acc1 + acc2 / 128).  IMMA k-step j (32 of d):
+      // b0 = q[head][16c + 4j .. +3], b1 = q[head][64 + 16c + 4j .. +3], stored as
+      // qf[nt][2j] = term 1 (b0, b1), qf[nt][2j + 1] = term 2.
+      const float s1 = amax / 127.0f;
+      const float inv1 = amax > 0.0f ? 127.0f / amax : 0.0f;
+      qscale = p.sm_scale_log2 * s1;
 #pragma unroll
-    for (int nt = 0; nt < NT; ++nt)
+      for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const uint32_t w[4] = {raw[nt][u].x, raw[nt][u].y, raw[nt][u].z, raw[nt][u].w};
-        uint32_t hw[4];
+        for (int jj = 0; jj < 4; ++jj)
 #pragma unroll
-        for (int e = 0; e < 4; ++e)
-          hw[e] = pack_half2(__uint_as_float(w[e] << 16) * pre,
-                             __uint_as_float(w[e] & 0xffff0000u) * pre);
-        const int i0 = 2 * u;  // uint4 u holds d = base(i0) .. base(i0) + 7
-        qf[nt][i0][0] = hw[0];
-        qf[nt][i0][1] = hw[1];
-        qf[nt][i0 + 1][0] = hw[2];
-        qf[nt][i0 + 1][1] = hw[3];
-      }
-  }
-  // INT8 K is fed to the MMA as code + 1152 (no HSUB2): S^T' = S^T + 1152 * sum_d q'.
-  // kbias[nt][e] = 1152 * sum_d q'[head 8nt + 2c + e][d], from the f16 values the MMA sees.
-  float kbias[NT][2];
+          for (int half = 0; half < 2; ++half) {
+            // 4 bf16 at d = (half ? 64 : 0) + 16c + 4jj: raw[nt][2*half + jj/2], words 2*(jj&1), +1
+            const uint4 rw = raw[nt][2 * half + (jj >> 1)];
+            const uint32_t wa = (jj & 1) ? rw.z : rw.x, wb = (jj & 1) ? rw.w : rw.y;
+            const float v[4] = {__uint_as_float(wa << 16), __uint_as_float(wa & 0xffff0000u),
+                                __uint_as_float(wb << 16), __uint_as_float(wb & 0xffff0000u)};
+            int t1[4], t2[4];
 #pragma unroll
-  for (int nt = 0; nt < NT; ++nt) {
-    float qs = 0.0f;
-    if (KVD == KVQ_INT8) {
+            for (int e = 0; e < 4; ++e) {
+              t1[e] = max(-127, min(127, __float2int_rn(v[e] * inv1)));
+              const float res = fmaf(-(float)t1[e], s1, v[e]);
+              t2[e] = max(-127, min(127, __float2int_rn(res * inv1 * 128.0f)));
+            }
+            qf[nt][2 * jj][half] = pack_s8x4(t1[0], t1[1], t1[2], t1[3]);
+            qf[nt][2 * jj + 1][half] = pack_s8x4(t2[0], t2[1], t2[2], t2[3]);
+          }
+    } else {
+      // Exact power-of-two prescale so max|q'| < 2^14 (fp16-safe); undone in qscale.
+      int ex = 0;
+      if (amax > 0.0f) frexpf(amax, &ex);
+      const float pre = pow2i(14 - ex);
+      qscale = p.sm_scale_log2 / pre;
 #pragma unroll
-      for (int i = 0; i < 8; ++i)
+      for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&qf[nt][i][e]));
-          qs += f.x + f.y;
+        for (int u = 0; u < 4; ++u) {
+          const uint32_t w[4] = {raw[nt][u].x, raw[nt][u].y, raw[nt][u].z, raw[nt][u].w};
+          uint32_t hw[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e)
+            hw[e] = pack_half2(__uint_as_float(w[e] << 16) * pre,
+                               __uint_as_float(w[e] & 0xffff0000u) * pre);
+          const int i0 = 2 * u;  // uint4 u holds d = base(i0) .. base(i0) + 7
+          qf[nt][i0][0] = hw[0];
+          qf[nt][i0][1] = hw[1];
+          qf[nt][i0 + 1][0] = hw[2];
+          qf[nt][i0 + 1][1] = hw[3];
         }
-      qs += __shfl_xor_sync(FULL, qs, 1);
-      qs += __shfl_xor_sync(FULL, qs, 2);
     }
-#pragma unroll
-    for (int e = 0; e < 2; ++e) kbias[nt][e] = 1152.0f * __shfl_sync(FULL, qs, 4 * (2 * c + e));
   }
-
   if (HI) {  // publish the (identical in every warp) fragments once per CTA
     if (warp == 0) {
 #pragma unroll
       for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
-        for (int i = 0; i < 8; ++i) qsm[(nt * 8 + i) * 32 + lane] = make_uint2(qf[nt][i][0], qf[nt][i][1]);
+        for (int i = 0; i < 8; i += 2)
+          reinterpret_cast<uint4*>(qsm)[(nt * 4 + i / 2) * 32 + lane] =
+              make_uint4(qf[nt][i][0], qf[nt][i][1], qf[nt][i + 1][0], qf[nt][i + 1][1]);
     }
     __syncthreads();
   }
 
   // Per-thread smem offsets inside a page (fixed for every page).
-  const int koff0 = r * 128 + ((c ^ ((r & 1) << 2)) << 4);         // token r, d [16c, 16c+16)
-  const int koff1 = r * 128 + (((c + 4) ^ ((r & 1) << 2)) << 4);   // token r, d [64+16c, ...)
-  const int koff2 = koff0 + 8 * 128;                                // token r+8 (same parity)
-  const int koff3 = koff1 + 8 * 128;
+  // K unit j of row pair r = {K[r][16c+4j..], K[r+8][16c+4j..], K[r][64+16c+4j..], K[r+8][64+16c+4j..]}
+  const int koff0 = r * 256 + (((0 + c) ^ ((r & 1) << 2)) << 4);
+  const int koff1 = r * 256 + (((4 + c) ^ ((r & 1) << 2)) << 4);
+  const int koff2 = r * 256 + (((8 + c) ^ ((r & 1) << 2)) << 4);
+  const int koff3 = r * 256 + (((12 + c) ^ ((r & 1) << 2)) << 4);
   const int R0 = 2 * c, R1 = 2 * c + 1;
   const int voff0 = V_OFF + R0 * 128 + ((r ^ (R0 & 7)) << 4);        // tokens 2c,2c+1 ; d [8r, 8r+8)
   const int voff1 = V_OFF + R1 * 128 + ((r ^ (R1 & 7)) << 4);        // d [64+8r, 64+8r+8)
@@ -548,94 +579,130 @@ __global__ void __launch_bounds__(THREADS, Geo<HI>::CTAS) decode_kernel(const De
     float ks_r = lds32f(pg + KS_OFF + 4 * r), ks_r8 = lds32f(pg + KS_OFF + 32 + 4 * r);
     float vs_r = lds32f(pg + VS_OFF + 4 * r), vs_r8 = lds32f(pg + VS_OFF + 32 + 4 * r);
 
-    // ---- S^T = K . Q^T : two accumulator chains per n-tile (k-steps 0-3, 4-7)
-    // The INT8 K bias (kbias) seeds the accumulator, so no separate subtraction.
-    // g <= 8: two chains (k-steps 0-3 / 4-7) for ILP; g > 8: the two n-tiles interleave.
+    // ---- S^T = K . Q^T
+    //   INT8: s8 tensor cores on the raw codes, two Q terms (acc1, acc2), 4 k-steps of 32.
+    //   FP8 : codes -> f16 (exact), 8 k-steps of 16; g <= 8 uses two chains for ILP.
     constexpr bool TWO_CHAINS = !HI;
-    float sa[NT][4], sb[NT][4];
-#pragma unroll
-    for (int nt = 0; nt < NT; ++nt) {
-      sa[nt][0] = sa[nt][2] = -kbias[nt][0];
-      sa[nt][1] = sa[nt][3] = -kbias[nt][1];
-#pragma unroll
-      for (int e = 0; e < 4; ++e) sb[nt][e] = 0.0f;
-    }
+    float st[NT][4];
     {
-      const uint32_t kr[8] = {k0.x, k0.y, k0.z, k0.w, k1.x, k1.y, k1.z, k1.w};
-      const uint32_t kr8[8] = {k2.x, k2.y, k2.z, k2.w, k3.x, k3.y, k3.z, k3.w};
+      // kr[i] / kr8[i]: 4 codes of token r / r+8 at d = base(i) .. base(i) + 3
+      const uint32_t kr[8] = {k0.x, k1.x, k2.x, k3.x, k0.z, k1.z, k2.z, k3.z};
+      const uint32_t kr8[8] = {k0.y, k1.y, k2.y, k3.y, k0.w, k1.w, k2.w, k3.w};
+      uint4 qpair[NT];
+      if constexpr (KVD == KVQ_INT8) {
+        int acc1[NT][4], acc2[NT][4];
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        uint32_t a0, a2, a1, a3;
-        codes_to_f16x2<KVD, true>(kr[i], a0, a2);
-        codes_to_f16x2<KVD, true>(kr8[i], a1, a3);
+        for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
-        for (int nt = 0; nt < NT; ++nt) {
-          uint32_t b0, b1;
-          if constexpr (HI) {
-            asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];"
-                         : "=r"(b0), "=r"(b1)
-                         : "r"(smem_u32(qsm + (nt * 8 + i) * 32 + lane)));
-          } else {
-            b0 = qf[nt][i][0];
-            b1 = qf[nt][i][1];
+          for (int e = 0; e < 4; ++e) acc1[nt][e] = acc2[nt][e] = 0;
+#pragma unroll
+        for (int jj = 0; jj < 4; ++jj) {
+#pragma unroll
+          for (int nt = 0; nt < NT; ++nt) {
+            uint32_t t1b0, t1b1, t2b0, t2b1;
+            if constexpr (HI) {
+              qpair[nt] = lds128(reinterpret_cast<const uint8_t*>(
+                  reinterpret_cast<const uint4*>(qsm) + (nt * 4 + jj) * 32 + lane));
+              t1b0 = qpair[nt].x; t1b1 = qpair[nt].y; t2b0 = qpair[nt].z; t2b1 = qpair[nt].w;
+            } else {
+              t1b0 = qf[nt][2 * jj][0]; t1b1 = qf[nt][2 * jj][1];
+              t2b0 = qf[nt][2 * jj + 1][0]; t2b1 = qf[nt][2 * jj + 1][1];
+            }
+            mma16832_s8(acc1[nt], kr[jj], kr8[jj], kr[4 + jj], kr8[4 + jj], t1b0, t1b1);
+            mma16832_s8(acc2[nt], kr[jj], kr8[jj], kr[4 + jj], kr8[4 + jj], t2b0, t2b1);
           }
-          mma16816((TWO_CHAINS && i >= 4) ? sb[nt] : sa[nt], a0, a1, a2, a3, b0, b1);
         }
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+          for (int e = 0; e < 4; ++e)
+            st[nt][e] = fmaf(__int2float_rn(acc2[nt][e]), 0.0078125f, __int2float_rn(acc1[nt][e]));
+      } else {
+        float sa[NT][4], sb[NT][4];
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+          for (int e = 0; e < 4; ++e) sa[nt][e] = sb[nt][e] = 0.0f;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          uint32_t a0, a2, a1, a3;
+          codes_to_f16x2<KVD>(kr[i], a0, a2);
+          codes_to_f16x2<KVD>(kr8[i], a1, a3);
+#pragma unroll
+          for (int nt = 0; nt < NT; ++nt) {
+            uint32_t b0, b1;
+            if constexpr (HI) {
+              if ((i & 1) == 0) qpair[nt] = lds128(reinterpret_cast<const uint8_t*>(
+                                    reinterpret_cast<const uint4*>(qsm) + (nt * 4 + i / 2) * 32 + lane));
+              b0 = (i & 1) ? qpair[nt].z : qpair[nt].x;
+              b1 = (i & 1) ? qpair[nt].w : qpair[nt].y;
+            } else {
+              b0 = qf[nt][i][0];
+              b1 = qf[nt][i][1];
+            }
+            mma16816((TWO_CHAINS && i >= 4) ? sb[nt] : sa[nt], a0, a1, a2, a3, b0, b1);
+          }
+        }
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+          for (int e = 0; e < 4; ++e) st[nt][e] = TWO_CHAINS ? sa[nt][e] + sb[nt][e] : sa[nt][e];
       }
     }
     if (HI) {  // g > 8: load V only after QK^T retired (keeps the live set under 128 regs)
       uint32_t dep;
-      asm volatile("mov.b32 %0, 0;" : "=r"(dep) : "f"(sa[0][0]), "f"(sa[NT - 1][3]));
+      asm volatile("mov.b32 %0, 0;" : "=r"(dep) : "f"(st[0][0]), "f"(st[NT - 1][3]));
       v0 = lds128(pg + voff0 + dep), v1 = lds128(pg + voff1 + dep);
       v2 = lds128(pg + voff2 + dep), v3 = lds128(pg + voff3 + dep);
     }
-    // ---- scores in log2 units; thread holds tokens r, r+8 x heads 2c, 2c+1 per n-tile
+    // ---- scores relative to the running max, log2 units: u = S^T * scale_k * qscale - m
+    //      (one FFMA); thread holds tokens r, r+8 x heads 2c, 2c+1 per n-tile.
     const int tok_base = (pg0 + warp + j * NW) * BS;
     const bool tail = tok_base + BS > L;
     const bool ok_r = !tail || tok_base + r < L, ok_r8 = !tail || tok_base + r + 8 < L;
     if (!ok_r) vs_r = 0.0f;
     if (!ok_r8) vs_r8 = 0.0f;
     const float kq_r = ks_r * qscale, kq_r8 = ks_r8 * qscale;
-    float sc[NT][4];  // [0]=(r,2c) [1]=(r,2c+1) [2]=(r+8,2c) [3]=(r+8,2c+1)
-    float mx[NT][2];
+    // st[nt]: [0]=(r,2c) [1]=(r,2c+1) [2]=(r+8,2c) [3]=(r+8,2c+1)
+    float u[NT][4];
+    bool over = false;
 #pragma unroll
     for (int nt = 0; nt < NT; ++nt) {
-      const float s0 = TWO_CHAINS ? sa[nt][0] + sb[nt][0] : sa[nt][0];
-      const float s1 = TWO_CHAINS ? sa[nt][1] + sb[nt][1] : sa[nt][1];
-      const float s2 = TWO_CHAINS ? sa[nt][2] + sb[nt][2] : sa[nt][2];
-      const float s3 = TWO_CHAINS ? sa[nt][3] + sb[nt][3] : sa[nt][3];
-      sc[nt][0] = ok_r ? s0 * kq_r : -INFINITY;
-      sc[nt][1] = ok_r ? s1 * kq_r : -INFINITY;
-      sc[nt][2] = ok_r8 ? s2 * kq_r8 : -INFINITY;
-      sc[nt][3] = ok_r8 ? s3 * kq_r8 : -INFINITY;
-      mx[nt][0] = fmaxf(sc[nt][0], sc[nt][2]);
-      mx[nt][1] = fmaxf(sc[nt][1], sc[nt][3]);
-    }
-    float vmax = fmaxf(vs_r, vs_r8);
 #pragma unroll
-    for (int o2 = 4; o2 <= 16; o2 <<= 1) {
-#pragma unroll
-      for (int nt = 0; nt < NT; ++nt) {
-        mx[nt][0] = fmaxf(mx[nt][0], __shfl_xor_sync(FULL, mx[nt][0], o2));
-        mx[nt][1] = fmaxf(mx[nt][1], __shfl_xor_sync(FULL, mx[nt][1], o2));
+      for (int q4 = 0; q4 < 4; ++q4) {
+        const bool ok = q4 < 2 ? ok_r : ok_r8;
+        u[nt][q4] = ok ? fmaf(st[nt][q4], q4 < 2 ? kq_r : kq_r8, -m[nt][q4 & 1]) : -INFINITY;
+        over |= hvalid[nt][q4 & 1] && u[nt][q4] > 8.0f;
       }
-      vmax = fmaxf(vmax, __shfl_xor_sync(FULL, vmax, o2));
     }
-    // ---- lazy rescale (threshold 2^8 for p, [2^-10, 2^4] for the V normaliser)
-    bool need = false;
-    bool nm[NT][2];
+    // ---- lazy rescale: p = 2^u must stay <= 2^8, and P' = p * scale_v * 2^E must
+    //      stay in f16 range (2^E keeps the page's max V scale in [2^-10, 2^4]).
+    //      Checked per thread + warp votes; the exact maxima (shuffle
+    //      reductions) are only computed on the rare pages that need a rescale.
+    const float ve_r = vs_r * escale, ve_r8 = vs_r8 * escale;
+    const bool trig = __any_sync(FULL, over || !escale_set || ve_r > 16.0f || ve_r8 > 16.0f) ||
+                      (__all_sync(FULL, ve_r < 0.0009765625f && ve_r8 < 0.0009765625f) &&
+                       __any_sync(FULL, vs_r > 0.0f || vs_r8 > 0.0f));
+    if (trig) {
+      float mx[NT][2];
 #pragma unroll
-    for (int nt = 0; nt < NT; ++nt)
+      for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        nm[nt][e] = hvalid[nt][e] && mx[nt][e] > m[nt][e] + 8.0f;
-        need |= nm[nt][e];
+        for (int e = 0; e < 2; ++e)
+          mx[nt][e] = fmaxf(ok_r ? st[nt][e] * kq_r : -INFINITY, ok_r8 ? st[nt][e + 2] * kq_r8 : -INFINITY);
+      float vmax = fmaxf(vs_r, vs_r8);
+#pragma unroll
+      for (int o2 = 4; o2 <= 16; o2 <<= 1) {
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+          mx[nt][0] = fmaxf(mx[nt][0], __shfl_xor_sync(FULL, mx[nt][0], o2));
+          mx[nt][1] = fmaxf(mx[nt][1], __shfl_xor_sync(FULL, mx[nt][1], o2));
+        }
+        vmax = fmaxf(vmax, __shfl_xor_sync(FULL, vmax, o2));
       }
-    const float ve = vmax * escale;
-    const bool need_e = vmax > 0.0f && (!escale_set || ve > 16.0f || ve < 0.0009765625f);
-    if (__any_sync(FULL, need || need_e)) {
+      const float ve = vmax * escale;
       float e_new = escale;
-      if (need_e) {
+      if (vmax > 0.0f && (!escale_set || ve > 16.0f || ve < 0.0009765625f)) {
         int ex;
         frexpf(vmax, &ex);
         e_new = pow2i(-ex);
@@ -648,8 +715,9 @@ __global__ void __launch_bounds__(THREADS, Geo<HI>::CTAS) decode_kernel(const De
         float f[2];
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
-          const float cl = nm[nt][e] ? fast_exp2(m[nt][e] - mx[nt][e]) : 1.0f;
-          if (nm[nt][e]) m[nt][e] = mx[nt][e];
+          const bool nm = hvalid[nt][e] && mx[nt][e] > m[nt][e] + 8.0f;
+          const float cl = nm ? fast_exp2(m[nt][e] - mx[nt][e]) : 1.0f;
+          if (nm) m[nt][e] = mx[nt][e];
           l[nt][e] *= cl;
           f[e] = cl * er;
         }
@@ -659,6 +727,11 @@ __global__ void __launch_bounds__(THREADS, Geo<HI>::CTAS) decode_kernel(const De
           o[nt][mt][1] *= f[1];
           o[nt][mt][2] *= f[0];
           o[nt][mt][3] *= f[1];
+        }
+#pragma unroll
+        for (int q4 = 0; q4 < 4; ++q4) {
+          const bool ok = q4 < 2 ? ok_r : ok_r8;
+          u[nt][q4] = ok ? fmaf(st[nt][q4], q4 < 2 ? kq_r : kq_r8, -m[nt][q4 & 1]) : -INFINITY;
         }
       }
     }
@@ -671,7 +744,7 @@ __global__ void __launch_bounds__(THREADS, Geo<HI>::CTAS) decode_kernel(const De
 #pragma unroll
       for (int q4 = 0; q4 < 4; ++q4) {
         const int e = q4 & 1;
-        pv[q4] = hvalid[nt][e] ? fast_exp2(sc[nt][q4] - m[nt][e]) : 0.0f;
+        pv[q4] = hvalid[nt][e] ? fast_exp2(u[nt][q4]) : 0.0f;
         l[nt][e] += pv[q4];
       }
       // 8x8 blocks: rows = tokens (r | r+8), cols = heads (2c, 2c+1)

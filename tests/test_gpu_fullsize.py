@@ -1,0 +1,97 @@
+"""Parity at BASELINE.json's full sizes.  The whole cache is written by K1 on
+the GPU, then (a) a seeded sample of sequences is checked against the CPU
+oracle on exactly those sequences' pages (same bytes, copied back), and
+(b) size-independent properties are checked on the full batch: split-KV
+invariance, determinism across launches, and head-major == transposed
+token-major output."""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+from paper_2605_29639_b200 import KVCacheSpec, PagedKVCache, paged_decode_attention, quantize_append
+
+pytestmark = [pytest.mark.gpu, pytest.mark.slow]
+
+
+def build(cuda, lens, Hq, Hkv, kv_dtype, seed):
+    lens = np.asarray(lens, dtype=np.int64)
+    B = len(lens)
+    nblk = np.ceil(lens / 16).astype(np.int64)
+    mb, nb = int(nblk.max()), int(nblk.sum())
+    rng = np.random.default_rng(seed)
+    perm = rng.permutation(nb).astype(np.int32)
+    table = np.zeros((B, mb), np.int32)
+    pos = 0
+    for b in range(B):
+        table[b, : nblk[b]] = perm[pos: pos + nblk[b]]
+        pos += nblk[b]
+    cache = PagedKVCache(KVCacheSpec(Hkv, kv_dtype=kv_dtype), nb, device=cuda)
+    gen = torch.Generator(device=cuda)
+    gen.manual_seed(seed)
+    tok_b = np.repeat(np.arange(B), lens)
+    tok_t = np.concatenate([np.arange(L) for L in lens])
+    slots = (table[tok_b, tok_t // 16].astype(np.int64) * 16 + tok_t % 16).astype(np.int32)
+    for s0 in range(0, len(slots), 1 << 16):
+        sl = torch.from_numpy(slots[s0: s0 + (1 << 16)]).to(cuda)
+        kv = torch.randn((2, sl.numel(), Hkv, 128), device=cuda, generator=gen)
+        kv = (kv * torch.exp(0.5 * torch.randn((2, sl.numel(), Hkv, 1), device=cuda, generator=gen)))
+        quantize_append(cache, kv[0].to(torch.bfloat16), kv[1].to(torch.bfloat16), sl)
+    q = torch.randn((B, Hq, 128), device=cuda, generator=gen).to(torch.bfloat16)
+    return cache, table, lens, q
+
+
+def oracle_subset(cache, table, lens, q, idx, Hkv, kvo):
+    """Oracle on sequences idx: copy their pages back, remap block ids."""
+    rows = table[idx]
+    used = np.unique(np.concatenate([rows[i, : math.ceil(lens[b] / 16)] for i, b in enumerate(idx)]))
+    remap = {int(b): i for i, b in enumerate(used)}
+    pages = cache.pool[torch.as_tensor(used, device=cache.device)].cpu().numpy()
+    t2 = np.zeros_like(rows)
+    for i, b in enumerate(idx):
+        n = math.ceil(lens[b] / 16)
+        t2[i, :n] = [remap[int(x)] for x in rows[i, :n]]
+    qb = q[torch.as_tensor(idx, device=q.device)].cpu().contiguous().view(torch.int16).numpy().view(np.uint16)
+    return O.decode_attn(qb, pages, t2, lens[idx].astype(np.int32), Hkv, kvo)
+
+
+def check(out, ref):
+    err = np.abs(out - ref).max(axis=-1)
+    scale = np.abs(ref).max(axis=-1)
+    assert np.isfinite(out).all()
+    assert (err <= 2e-3 * scale + 1e-6).all(), float((err / (scale + 1e-9)).max())
+
+
+@pytest.mark.parametrize("name", ["c2", "c3_1gpu"])
+def test_full_size_sampled_parity_and_properties(cuda, name):
+    if name == "c2":
+        lens = np.random.default_rng(3).integers(512, 8193, size=256) + 1
+        Hq, Hkv, kvd, kvo = 32, 8, "int8", O.INT8
+    else:
+        lens = np.full(128, 32769)
+        Hq, Hkv, kvd, kvo = 64, 8, "fp8_e4m3", O.FP8_E4M3
+    cache, table, lens, q = build(cuda, lens, Hq, Hkv, kvd, seed=11)
+    tab = torch.from_numpy(table).to(cuda)
+    sl = torch.from_numpy(lens.astype(np.int32)).to(cuda)
+    out = paged_decode_attention(q, cache, tab, sl, out_dtype=torch.float32)
+    out2 = paged_decode_attention(q, cache, tab, sl, out_dtype=torch.float32)
+    assert torch.equal(out, out2), "deterministic across launches"
+    hm = paged_decode_attention(q, cache, tab, sl, out_dtype=torch.float32, head_major=True)
+    assert torch.equal(hm.transpose(0, 1), out)
+    alt = paged_decode_attention(q, cache, tab, sl, out_dtype=torch.float32, pages_per_split=13)
+    o, a = out.cpu().numpy(), alt.cpu().numpy()
+    assert (np.abs(o - a).max(-1) <= 2e-3 * np.abs(o).max(-1) + 1e-6).all(), "split invariance"
+    idx = np.random.default_rng(0).choice(len(lens), size=6 if name == "c2" else 2, replace=False)
+    check(o[idx], oracle_subset(cache, table, lens, q, idx, Hkv, kvo))
+
+
+def test_c4_shape_128k_context(cuda):
+    """Qwen3-235B shape (g = 16), INT8, 128K context: two sequences checked
+    against the oracle end to end."""
+    lens = np.array([131073, 100000])
+    cache, table, lens, q = build(cuda, lens, 64, 4, "int8", seed=12)
+    out = paged_decode_attention(q, cache, torch.from_numpy(table).to(cuda),
+                                 torch.from_numpy(lens.astype(np.int32)).to(cuda), out_dtype=torch.float32)
+    check(out.cpu().numpy(), oracle_subset(cache, table, lens, q, np.arange(2), 4, O.INT8))

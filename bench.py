@@ -296,7 +296,8 @@ def run_ours(args, cfg):
         return OutputGather(plan, Hq, B, torch.bfloat16, dev)
 
     sess = DecodeSession(cache, table_d, B_loc, Hq_loc, total_pages=total_pages, head_major=True,
-                         gather_factory=make_gather if world > 1 else None)
+                         gather_factory=make_gather if world > 1 else None,
+                         pages_per_split=args.pages_per_split)
     buf = sess.device_buffers(0)
     for name, t in (("q", q), ("k", k_new), ("v", v_new), ("slots", slots_step), ("lens", seq_lens_d)):
         buf[name].copy_(t)
@@ -593,6 +594,8 @@ def main(argv=None):
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--pages-per-split", type=int, default=None,
+                    help="override the split-KV geometry (default: kvq_decode_pages_per_split)")
     ap.add_argument("--kv", default=None, choices=["int8", "fp8_e4m3"],
                     help="override the config's KV dtype (the C5 INT8 vs FP8 sweep)")
     args = ap.parse_args(argv)

@@ -53,58 +53,89 @@ __host__ __device__ __forceinline__ int v_code_off(int tok, int d) {
 }
 
 // ---------------------------------------------------------------------------
-// K1: quantize-on-append.  CTA = 16 consecutive tokens x one kv head; warp w
-// quantizes tokens 2w, 2w+1 (K and V rows: 4 rows, loads issued first).
-// When the 16 tokens fill one whole page (slots blk*16 + 0..15, the chunked-
-// prefill case) the page image is assembled in shared memory and written
-// with coalesced 16-byte stores; otherwise each row is scattered directly
-// (decode: one token per sequence).
+// K1: quantize-on-append.  CTA = 16 consecutive tokens x 4 kv heads; an
+// 8-lane group owns one (token pair 2p/2p+1, head): its 4 rows (K and V of
+// both tokens, 16 elements per lane) are loaded up front with LDG.128, reduced
+// over 8 lanes, and written
+//   * as a whole page image in shared memory, then 16-byte coalesced stores,
+//     when the 16 tokens fill one page (slots blk*16 + 0..15: chunked prefill);
+//   * directly otherwise (decode: one token per sequence), V as interleaved
+//     16-byte chunks when the pair's two slots are adjacent, else byte-wise.
 // ---------------------------------------------------------------------------
-constexpr int K1_WARPS = 8;
+constexpr int K1_THREADS = 256;
+constexpr int K1_HEADS = 4;
 
+// Quantize 16 values held by this lane of an 8-lane row group (contract).
 template <int KVD>
-__device__ __forceinline__ uint32_t quantize4(const uint2 raw, float& scale_out) {
-  float x[4];
-  x[0] = __uint_as_float(raw.x << 16);
-  x[1] = __uint_as_float(raw.x & 0xffff0000u);
-  x[2] = __uint_as_float(raw.y << 16);
-  x[3] = __uint_as_float(raw.y & 0xffff0000u);
-  float a = fmaxf(fmaxf(fabsf(x[0]), fabsf(x[1])), fmaxf(fabsf(x[2]), fabsf(x[3])));
+__device__ __forceinline__ void quantize16(const uint4 lo, const uint4 hi, float& scale_out,
+                                           uint32_t (&codes)[4]) {
+  float x[16];
+  const uint32_t w[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) a = fmaxf(a, __shfl_xor_sync(FULL, a, o));
+  for (int i = 0; i < 8; ++i) {
+    x[2 * i] = __uint_as_float(w[i] << 16);
+    x[2 * i + 1] = __uint_as_float(w[i] & 0xffff0000u);
+  }
+  float a = 0.0f;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) a = fmaxf(a, fabsf(x[i]));
+#pragma unroll
+  for (int o = 1; o < 8; o <<= 1) a = fmaxf(a, __shfl_xor_sync(FULL, a, o));
   const float qmax = KVD == KVQ_FP8_E4M3 ? 448.0f : 127.0f;
-  // Contract: IEEE divisions, one RN multiply, no contraction.
   scale_out = __fdiv_rn(a, qmax);
   const float inv = a > 0.0f ? __fdiv_rn(qmax, a) : 0.0f;
-  float y[4];
 #pragma unroll
-  for (int e = 0; e < 4; ++e) y[e] = __fmul_rn(x[e], inv);
-  uint32_t word;
-  if constexpr (KVD == KVQ_FP8_E4M3) {
-    uint16_t lo, hi;
-    asm("cvt.rn.satfinite.e4m3x2.f32 %0, %1, %2;" : "=h"(lo) : "f"(y[1]), "f"(y[0]));
-    asm("cvt.rn.satfinite.e4m3x2.f32 %0, %1, %2;" : "=h"(hi) : "f"(y[3]), "f"(y[2]));
-    word = (uint32_t)lo | ((uint32_t)hi << 16);
-  } else {
-    word = 0;
+  for (int i = 0; i < 4; ++i) {
+    float y[4];
 #pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      int c = __float2int_rn(y[e]);  // cvt.rni.s32.f32: NaN -> 0, saturating
-      c = max(-127, min(127, c));
-      word |= ((uint32_t)(c & 0xff)) << (8 * e);
+    for (int e = 0; e < 4; ++e) y[e] = __fmul_rn(x[4 * i + e], inv);
+    if constexpr (KVD == KVQ_FP8_E4M3) {
+      uint16_t l, h;
+      asm("cvt.rn.satfinite.e4m3x2.f32 %0, %1, %2;" : "=h"(l) : "f"(y[1]), "f"(y[0]));
+      asm("cvt.rn.satfinite.e4m3x2.f32 %0, %1, %2;" : "=h"(h) : "f"(y[3]), "f"(y[2]));
+      codes[i] = (uint32_t)l | ((uint32_t)h << 16);
+    } else {
+      uint32_t word = 0;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int c = max(-127, min(127, __float2int_rn(y[e])));  // NaN -> 0, saturating
+        word |= ((uint32_t)(c & 0xff)) << (8 * e);
+      }
+      codes[i] = word;
     }
   }
-  return word;
 }
 
 template <int KVD>
-__global__ void __launch_bounds__(32 * K1_WARPS) quant_append_kernel(
+__global__ void __launch_bounds__(K1_THREADS) quant_append_kernel(
     const __nv_bfloat16* __restrict__ k, const __nv_bfloat16* __restrict__ v, int64_t k_stride,
     int64_t v_stride, const int32_t* __restrict__ slots, int T, int Hkv,
     uint8_t* __restrict__ pool, int64_t num_blocks) {
-  __shared__ __align__(16) uint8_t img[PAGE];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int t0 = blockIdx.x * 16, h = blockIdx.y;
+  __shared__ __align__(16) uint8_t img[K1_HEADS][PAGE];
+  const int t0 = blockIdx.x * 16, h0 = blockIdx.y * K1_HEADS;
+  const int grp = threadIdx.x >> 3, j = threadIdx.x & 7;  // lane j of the group owns d [16j, 16j+16)
+  const int hh = grp >> 3, pp = grp & 7;                  // head h0+hh, tokens t0+2pp, t0+2pp+1
+  const int h = h0 + hh;
+  // Row loads first (they do not depend on the slots), then the slot loads.
+  uint4 raw[2][2][2];  // [token][K|V][lo|hi 16 B]
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const int t = t0 + 2 * pp + i;
+    const bool in = t < T && h < Hkv;
+#pragma unroll
+    for (int kv = 0; kv < 2; ++kv) {
+      const __nv_bfloat16* src = (kv ? v + (int64_t)t * v_stride : k + (int64_t)t * k_stride) + h * HD + 16 * j;
+      raw[i][kv][0] = in ? __ldg(reinterpret_cast<const uint4*>(src)) : make_uint4(0, 0, 0, 0);
+      raw[i][kv][1] = in ? __ldg(reinterpret_cast<const uint4*>(src + 8)) : make_uint4(0, 0, 0, 0);
+    }
+  }
+  int slot[2];
+  bool live[2];
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const int t = t0 + 2 * pp + i;
+    slot[i] = t < T ? __ldg(slots + t) : -1;
+  }
   // Whole-page test: 16 in-range tokens with slots blk*16 + 0..15.
   int my_slot = -1;
   if (threadIdx.x < 16 && t0 + threadIdx.x < T) my_slot = __ldg(slots + t0 + threadIdx.x);
@@ -113,40 +144,62 @@ __global__ void __launch_bounds__(32 * K1_WARPS) quant_append_kernel(
                        (my_slot >= 0 && my_slot == first + (int)threadIdx.x && (first & 15) == 0 &&
                         (first >> 4) < num_blocks);
   const bool whole = __syncthreads_and(mine_ok);
+#pragma unroll
+  for (int i = 0; i < 2; ++i) live[i] = slot[i] >= 0 && (slot[i] >> 4) < num_blocks && h < Hkv;
+  uint32_t code[2][2][4];
+  float scale[2][2];
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int kv = 0; kv < 2; ++kv) quantize16<KVD>(raw[i][kv][0], raw[i][kv][1], scale[i][kv], code[i][kv]);
 
-  uint2 raw[4];
-  int slot[2];
+  const bool pair_adj = live[0] && live[1] && (slot[0] & 1) == 0 && slot[1] == slot[0] + 1;
 #pragma unroll
   for (int i = 0; i < 2; ++i) {
-    const int t = t0 + 2 * warp + i;
-    slot[i] = t < T ? __ldg(slots + t) : -1;
-    const bool live = slot[i] >= 0 && (slot[i] >> 4) < num_blocks;
-    raw[2 * i] = live ? __ldg(reinterpret_cast<const uint2*>(k + (int64_t)t * k_stride + h * HD + lane * 4))
-                      : make_uint2(0, 0);
-    raw[2 * i + 1] = live ? __ldg(reinterpret_cast<const uint2*>(v + (int64_t)t * v_stride + h * HD + lane * 4))
-                          : make_uint2(0, 0);
-  }
-#pragma unroll
-  for (int r4 = 0; r4 < 4; ++r4) {
-    const int i = r4 >> 1, kv = r4 & 1;
-    if (slot[i] < 0 || (slot[i] >> 4) >= num_blocks) continue;  // warp-uniform
+    if (!live[i]) continue;
     const int tok = slot[i] & 15;
-    float scale;
-    const uint32_t word = quantize4<KVD>(raw[r4], scale);
-    uint8_t* page = whole ? img : pool + ((int64_t)(slot[i] >> 4) * Hkv + h) * PAGE;
-    if (kv == 0) {
-      *reinterpret_cast<uint32_t*>(page + k_code_off(tok, lane * 4)) = word;
-    } else {
+    uint8_t* page = whole ? img[hh] : pool + ((int64_t)(slot[i] >> 4) * Hkv + h) * PAGE;
 #pragma unroll
-      for (int e = 0; e < 4; ++e) page[v_code_off(tok, lane * 4 + e)] = (uint8_t)(word >> (8 * e));
+    for (int w = 0; w < 4; ++w)
+      *reinterpret_cast<uint32_t*>(page + k_code_off(tok, 16 * j + 4 * w)) = code[i][0][w];
+    if (!(whole || pair_adj)) {  // lone token: V bytes at 2d + (tok & 1)
+#pragma unroll
+      for (int w = 0; w < 4; ++w)
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+          page[v_code_off(tok, 16 * j + 4 * w + e)] = (uint8_t)(code[i][1][w] >> (8 * e));
     }
-    if (lane == 0) *reinterpret_cast<float*>(page + (kv ? VS_OFF : KS_OFF) + 4 * tok) = scale;
+    if (j == 0) {
+      *reinterpret_cast<float*>(page + KS_OFF + 4 * tok) = scale[i][0];
+      *reinterpret_cast<float*>(page + VS_OFF + 4 * tok) = scale[i][1];
+    }
+  }
+  if (whole || pair_adj) {
+    // Interleave the pair's V codes: bytes (d, t0), (d, t1) for d = 16j .. 16j+15 form the
+    // logical pair-row range [32j, 32j+32) = two 16-byte chunks.
+    uint32_t il[8];
+#pragma unroll
+    for (int w = 0; w < 4; ++w) {
+      il[2 * w] = __byte_perm(code[0][1][w], code[1][1][w], 0x5140);
+      il[2 * w + 1] = __byte_perm(code[0][1][w], code[1][1][w], 0x7362);
+    }
+    const int tok = slot[0] & 15;  // even
+    uint8_t* page = whole ? img[hh] : pool + ((int64_t)(slot[0] >> 4) * Hkv + h) * PAGE;
+#pragma unroll
+    for (int half = 0; half < 2; ++half) {
+      const int dd = 16 * j + 8 * half;  // d of the chunk's first byte pair
+      *reinterpret_cast<uint4*>(page + v_code_off(tok, dd)) =
+          make_uint4(il[4 * half], il[4 * half + 1], il[4 * half + 2], il[4 * half + 3]);
+    }
   }
   if (whole) {
     __syncthreads();
-    uint4* dst = reinterpret_cast<uint4*>(pool + ((int64_t)(first >> 4) * Hkv + h) * PAGE);
-    const uint4* src = reinterpret_cast<const uint4*>(img);
-    for (int i = threadIdx.x; i < PAGE / 16; i += 32 * K1_WARPS) dst[i] = src[i];
+    const int nh = min(K1_HEADS, Hkv - h0);
+    for (int x = 0; x < nh; ++x) {
+      uint4* dst = reinterpret_cast<uint4*>(pool + ((int64_t)(first >> 4) * Hkv + h0 + x) * PAGE);
+      const uint4* src = reinterpret_cast<const uint4*>(img[x]);
+      for (int i = threadIdx.x; i < PAGE / 16; i += K1_THREADS) dst[i] = src[i];
+    }
   }
 }
 
@@ -970,14 +1023,26 @@ int kvq_quant_append(const void* k, const void* v, int64_t k_token_stride, int64
     return fail(KVQ_EUNSUPPORTED, "quant_append: unknown kv dtype");
   if (int rc = check_device()) return rc;
   if (Hkv > 65535) return fail(KVQ_EINVAL, "quant_append: Hkv too large");
-  const dim3 grid((unsigned)((T + 15) / 16), (unsigned)Hkv);
+  const dim3 grid((unsigned)((T + 15) / 16), (unsigned)((Hkv + kvq::K1_HEADS - 1) / kvq::K1_HEADS));
   auto st = static_cast<cudaStream_t>(stream);
+  // Same (max-shared) L1/smem carveout as K2 so a decode step never pays an
+  // SM reconfiguration between the append and the attention kernel.
+  static const bool carve = [] {
+    cudaFuncSetAttribute(kvq::quant_append_kernel<KVQ_INT8>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                         cudaSharedmemCarveoutMaxShared);
+    cudaFuncSetAttribute(kvq::quant_append_kernel<KVQ_FP8_E4M3>,
+                         cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
+    cudaFuncSetAttribute(kvq::copy_blocks_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
+                         cudaSharedmemCarveoutMaxShared);
+    return true;
+  }();
+  (void)carve;
   if (kv_dtype == KVQ_INT8)
-    kvq::quant_append_kernel<KVQ_INT8><<<grid, 32 * kvq::K1_WARPS, 0, st>>>(
+    kvq::quant_append_kernel<KVQ_INT8><<<grid, kvq::K1_THREADS, 0, st>>>(
         static_cast<const __nv_bfloat16*>(k), static_cast<const __nv_bfloat16*>(v), k_token_stride,
         v_token_stride, slot_mapping, T, Hkv, static_cast<uint8_t*>(pool), num_blocks);
   else
-    kvq::quant_append_kernel<KVQ_FP8_E4M3><<<grid, 32 * kvq::K1_WARPS, 0, st>>>(
+    kvq::quant_append_kernel<KVQ_FP8_E4M3><<<grid, kvq::K1_THREADS, 0, st>>>(
         static_cast<const __nv_bfloat16*>(k), static_cast<const __nv_bfloat16*>(v), k_token_stride,
         v_token_stride, slot_mapping, T, Hkv, static_cast<uint8_t*>(pool), num_blocks);
   return check_launch("quant_append");
@@ -994,7 +1059,6 @@ size_t kvq_decode_workspace_bytes(int32_t B, int32_t Hq, int32_t Hkv, int32_t ma
 int32_t kvq_decode_pages_per_split(int32_t B, int32_t Hkv, int64_t total_pages, int32_t max_blocks) {
   // Uniform splits of <= 64 pages (270 KB of KV per CTA) so the ragged tail is
   // at most one short CTA; as few waves of CTAs_PER_SM x SMs as that allows.
-  (void)B;
   int sms = 148, dev = 0;
   if (cudaGetDevice(&dev) == cudaSuccess) {
     int v = 0;
@@ -1006,6 +1070,10 @@ int32_t kvq_decode_pages_per_split(int32_t B, int32_t Hkv, int64_t total_pages, 
   const int64_t work = total_pages * (int64_t)Hkv;
   const int64_t waves = (work + slots * 64 - 1) / (slots * 64);
   int64_t pps = (work + slots * (waves > 0 ? waves : 1) - 1) / (slots * (waves > 0 ? waves : 1));
+  // Single wave: leave room for each (sequence, head)'s rounded-up last split so
+  // the grid really fits one wave (a second, nearly empty wave doubles latency).
+  const int64_t pairs = (int64_t)B * Hkv;
+  if (waves <= 1 && slots > pairs) pps = (work + (slots - pairs) - 1) / (slots - pairs);
   if (pps < 8) pps = 8;
   if (pps > 64) pps = 64;
   if (max_blocks > 0 && pps > max_blocks) pps = max_blocks;

@@ -33,7 +33,7 @@ class DecodeSession:
     def __init__(self, cache: PagedKVCache, block_table: torch.Tensor, batch: int, num_q_heads: int,
                  *, total_pages: Optional[int] = None, out_dtype: torch.dtype = torch.bfloat16,
                  head_major: bool = False, sm_scale: Optional[float] = None, depth: int = 2,
-                 gather_factory=None):
+                 gather_factory=None, pages_per_split: Optional[int] = None):
         """With ``gather_factory`` (returning a
         :class:`paper_2605_29639_b200.shard.OutputGather`, one per buffer slot,
         for KV-head / 2-D sharding) the local head-major output
@@ -48,7 +48,7 @@ class DecodeSession:
         self.head_major, self.sm_scale, self.out_dtype = head_major, sm_scale, out_dtype
         lib = _lib.load()
         max_blocks = block_table.shape[1]
-        self.pps = int(lib.kvq_decode_pages_per_split(
+        self.pps = int(pages_per_split or lib.kvq_decode_pages_per_split(
             batch, self.Hkv, total_pages if total_pages is not None else batch * max_blocks, max_blocks))
         max_splits = -(-max_blocks // self.pps)
         self.depth = depth

@@ -936,8 +936,10 @@ __global__ void __launch_bounds__(THREADS, Geo<HI>::CTAS) decode_kernel(const De
     const int head = h * g + row;
     const int64_t base = ((int64_t)b * p.Hq + head) * p.max_splits;
     float M = -INFINITY;
+#pragma unroll 4
     for (int sp = 0; sp < nsplit; ++sp) M = fmaxf(M, __ldcg(p.part_lse + base + sp));
     float wsum = 0.0f, acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#pragma unroll 4
     for (int sp = 0; sp < nsplit; ++sp) {
       const float wgt = fast_exp2(__ldcg(p.part_lse + base + sp) - M);
       wsum += wgt;
@@ -1068,14 +1070,18 @@ int32_t kvq_decode_pages_per_split(int32_t B, int32_t Hkv, int64_t total_pages, 
   }
   const int64_t slots = (int64_t)sms * kvq::CTAS_PER_SM;
   const int64_t work = total_pages * (int64_t)Hkv;
-  const int64_t waves = (work + slots * 64 - 1) / (slots * 64);
+  // Equal-length batches have no ragged tail to protect: allow 256-page
+  // splits (4x less split prologue / partial traffic / combine work).
+  const bool uniform = max_blocks > 0 && total_pages * 20 >= (int64_t)B * max_blocks * 19;
+  const int64_t cap = uniform ? 256 : 64;
+  const int64_t waves = (work + slots * cap - 1) / (slots * cap);
   int64_t pps = (work + slots * (waves > 0 ? waves : 1) - 1) / (slots * (waves > 0 ? waves : 1));
   // Single wave: leave room for each (sequence, head)'s rounded-up last split so
   // the grid really fits one wave (a second, nearly empty wave doubles latency).
   const int64_t pairs = (int64_t)B * Hkv;
   if (waves <= 1 && slots > pairs) pps = (work + (slots - pairs) - 1) / (slots - pairs);
   if (pps < 8) pps = 8;
-  if (pps > 64) pps = 64;
+  if (pps > cap) pps = cap;
   if (max_blocks > 0 && pps > max_blocks) pps = max_blocks;
   return (int32_t)(pps > 0 ? pps : 1);
 }

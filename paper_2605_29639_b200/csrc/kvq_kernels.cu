@@ -917,9 +917,10 @@ __global__ void __launch_bounds__(THREADS, Geo<HI>::CTAS) decode_kernel(const De
   if (nsplit == 1) return;
 
   // ===== fused split-KV combine: the last CTA of (b, h) merges all splits =====
-  // bar.sync orders the CTA's partial stores before thread 0's acq_rel atomic
-  // (release at gpu scope, cumulative); the last arriver's acquire + bar.sync
-  // make every split's partials visible to its threads.
+  // Every thread fences its partial stores at gpu scope before the barrier;
+  // thread 0's acq_rel atomic then publishes the split, and the last
+  // arriver's acquire + bar.sync make every split's partials visible.
+  __threadfence();
   __syncthreads();
   if (tid == 0) {
     int* ctr = p.counters + (int64_t)b * p.Hkv + h;
@@ -1059,7 +1060,7 @@ size_t kvq_decode_workspace_bytes(int32_t B, int32_t Hq, int32_t Hkv, int32_t ma
 }
 
 int32_t kvq_decode_pages_per_split(int32_t B, int32_t Hkv, int64_t total_pages, int32_t max_blocks) {
-  // Uniform splits of <= 64 pages (270 KB of KV per CTA) so the ragged tail is
+  // Uniform splits of <= 128 pages (540 KB of KV per CTA) so the ragged tail is
   // at most one short CTA; as few waves of CTAs_PER_SM x SMs as that allows.
   int sms = 148, dev = 0;
   if (cudaGetDevice(&dev) == cudaSuccess) {
@@ -1070,10 +1071,10 @@ int32_t kvq_decode_pages_per_split(int32_t B, int32_t Hkv, int64_t total_pages, 
   }
   const int64_t slots = (int64_t)sms * kvq::CTAS_PER_SM;
   const int64_t work = total_pages * (int64_t)Hkv;
-  // Equal-length batches have no ragged tail to protect: allow 256-page
+  // Equal-length batches have no ragged tail to protect: allow 512-page
   // splits (4x less split prologue / partial traffic / combine work).
   const bool uniform = max_blocks > 0 && total_pages * 20 >= (int64_t)B * max_blocks * 19;
-  const int64_t cap = uniform ? 256 : 64;
+  const int64_t cap = uniform ? 512 : 128;
   const int64_t waves = (work + slots * cap - 1) / (slots * cap);
   int64_t pps = (work + slots * (waves > 0 ? waves : 1) - 1) / (slots * (waves > 0 ? waves : 1));
   // Single wave: leave room for each (sequence, head)'s rounded-up last split so

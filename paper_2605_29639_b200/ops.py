@@ -17,7 +17,7 @@ import torch
 from . import _lib
 from .cache import PagedKVCache
 
-_WS_CACHE: Dict[Tuple[int, int], torch.Tensor] = {}
+_WS_CACHE: Dict[Tuple[int, int], list] = {}
 
 
 def _stream_handle(device: torch.device) -> int:
@@ -64,14 +64,22 @@ def workspace_bytes(batch: int, num_q_heads: int, num_kv_heads: int, max_splits:
     return int(_lib.load().kvq_decode_workspace_bytes(batch, num_q_heads, num_kv_heads, max_splits))
 
 
-def _workspace(device: torch.device, nbytes: int) -> torch.Tensor:
+def _workspace(device: torch.device, nbytes: int, counter_bytes: int) -> torch.Tensor:
+    """Per-(device, stream) cached workspace.  Its first ``counter_bytes`` (the
+    split-combine arrival counters, offset 0) must be zero on entry; the kernel
+    leaves them zero, but a later call with a larger batch x kv-head count
+    moves the counter region over former partials, so that prefix is re-zeroed
+    whenever it grows."""
     key = (device.index if device.index is not None else torch.cuda.current_device(),
            _stream_handle(device))
-    ws = _WS_CACHE.get(key)
-    if ws is None or ws.numel() < nbytes:
-        ws = torch.zeros(max(nbytes, 1 << 20), dtype=torch.uint8, device=device)
-        _WS_CACHE[key] = ws
-    return ws
+    ent = _WS_CACHE.get(key)
+    if ent is None or ent[0].numel() < nbytes:
+        ent = [torch.zeros(max(nbytes, 1 << 20), dtype=torch.uint8, device=device), counter_bytes]
+        _WS_CACHE[key] = ent
+    elif counter_bytes > ent[1]:
+        ent[0][:counter_bytes].zero_()
+        ent[1] = counter_bytes
+    return ent[0]
 
 
 def paged_decode_attention(q: torch.Tensor, cache: PagedKVCache, block_table: torch.Tensor,
@@ -119,7 +127,7 @@ def paged_decode_attention(q: torch.Tensor, cache: PagedKVCache, block_table: to
     max_splits = -(-max_blocks // pps)
     nbytes = lib.kvq_decode_workspace_bytes(B, Hq, spec.num_kv_heads, max_splits)
     if workspace is None:
-        workspace = _workspace(q.device, nbytes)
+        workspace = _workspace(q.device, nbytes, ((B * spec.num_kv_heads * 4 + 255) // 256) * 256)
     elif workspace.numel() * workspace.element_size() < nbytes:
         raise ValueError(f"paged_decode_attention: workspace needs {nbytes} bytes")
     st = lib.kvq_decode_attn(

@@ -32,8 +32,8 @@ def test_library_exports_every_symbol():
 
 def test_host_only_entry_points():
     L = _lib.load()
-    # split geometry: <= 64 pages, >= 8 pages, <= max_blocks
-    assert L.kvq_decode_pages_per_split(256, 8, 70400, 513) == 64
+    # split geometry: <= 128 pages ragged (512 equal-length), >= 8 pages, <= max_blocks
+    assert 64 < L.kvq_decode_pages_per_split(256, 8, 70400, 513) <= 128
     assert 8 <= L.kvq_decode_pages_per_split(8, 8, 8 * 129, 129) <= 64
     assert L.kvq_decode_pages_per_split(1, 1, 3, 3) == 3
     ws = L.kvq_decode_workspace_bytes(4, 32, 8, 3)

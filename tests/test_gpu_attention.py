@@ -103,3 +103,25 @@ def test_append_then_attend_e2e(cuda, kv_dtype):
     out = paged_decode_attention(sc.q.to(cuda), cache, torch.from_numpy(sc.block_table).to(cuda),
                                  torch.from_numpy(sc.seq_lens).to(cuda), out_dtype=torch.float32)
     assert rel_err(out.cpu().numpy(), sc.oracle_out()) <= 2e-3
+
+
+@pytest.mark.parametrize("pps", [2, 5, 40])
+def test_split_combine_is_race_free(cuda, pps):
+    """The fused combine must read every split's finished partials: poison the
+    workspace, then repeat launches must be bit-identical to a clean run."""
+    sc = Scenario([900, 1700, 33, 2500, 1200, 64], 32, 8, O.INT8, seed=31)
+    cache = PagedKVCache(KVCacheSpec(8), sc.num_blocks, device=cuda, pool=torch.from_numpy(sc.pool).to(cuda))
+    args = (sc.q.to(cuda), cache, torch.from_numpy(sc.block_table).to(cuda), torch.from_numpy(sc.seq_lens).to(cuda))
+    from paper_2605_29639_b200 import ops
+    mb = sc.block_table.shape[1]
+    nbytes = ops.workspace_bytes(sc.B, 32, 8, -(-mb // pps))
+    ws = torch.zeros(nbytes, dtype=torch.uint8, device=cuda)
+    base = paged_decode_attention(*args, out_dtype=torch.float32, pages_per_split=pps, workspace=ws)
+    ref = sc.oracle_out()
+    assert rel_err(base.cpu().numpy(), ref) <= 2e-3
+    for trial in range(20):
+        # poison the partials (keep the zeroed arrival counters at the front)
+        cnt = 256 * ((sc.B * 8 * 4 + 255) // 256)
+        ws[cnt:].fill_(0x7F if trial % 2 else 0xFF)
+        again = paged_decode_attention(*args, out_dtype=torch.float32, pages_per_split=pps, workspace=ws)
+        assert torch.equal(again, base), f"trial {trial}"

@@ -419,7 +419,7 @@ def run_ours(args, cfg):
                            "stationary ctx; device steps replay CUDA graphs of K1 and K2",
                    "e2e": "DecodeSession.submit: H2D of q/k/v/slots/lens from pinned memory, K1, K2, "
                           "(all-gather), D2H of O; double-buffered copy streams overlap adjacent steps",
-                   "compute": "codes->f16 in registers, mma.sync m16n8k16 f16 x f16 -> f32"},
+                   "compute": "TMA bulk page copies; QK^T: INT8 codes on s8 tensor cores (mma m16n8k32, two-term int8 Q) / E4M3 codes -> f16 (mma m16n8k16); PV: codes -> f16, mma m16n8k16 f32 accumulate"},
         "hbm_gbs_algorithmic_step": (attn_bytes + append_bytes) / (ms_step * 1e-3) / 1e9,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "kernel": "kvq::decode_kernel",

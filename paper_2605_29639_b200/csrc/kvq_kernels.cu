@@ -463,6 +463,23 @@ __global__ void __launch_bounds__(THREADS, Geo<HI>::CTAS) decode_kernel(const De
   const int pg0 = split * p.pages_per_split;
   const int n = min(npages, pg0 + p.pages_per_split) - pg0;
 
+  // Q loads go out first: their latency overlaps the page-stream setup below.
+  uint4 raw[NT][4];
+  {
+    const int r = lane >> 2, c = lane & 3;
+    const __nv_bfloat16* qrow = p.q + (int64_t)b * p.q_stride_b + (int64_t)(h * g) * HD;
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) {
+      const bool valid = 8 * nt + r < g;
+      const __nv_bfloat16* src = qrow + (8 * nt + r) * HD;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int d = (u < 2 ? 16 * c + 8 * u : 64 + 16 * c + 8 * (u - 2));
+        raw[nt][u] = valid ? __ldg(reinterpret_cast<const uint4*>(src + d)) : make_uint4(0, 0, 0, 0);
+      }
+    }
+  }
+
   PageStream<S> ps;
   ps.bt = p.block_table + (int64_t)b * p.max_blocks + pg0;
   ps.head_base = p.pool + (int64_t)h * PAGE;
@@ -491,18 +508,6 @@ __global__ void __launch_bounds__(THREADS, Geo<HI>::CTAS) decode_kernel(const De
   uint32_t qf[NT][8][2];
   float qscale;
   {
-    const __nv_bfloat16* qrow = p.q + (int64_t)b * p.q_stride_b + (int64_t)(h * g) * HD;
-    uint4 raw[NT][4];
-#pragma unroll
-    for (int nt = 0; nt < NT; ++nt) {
-      const bool valid = 8 * nt + r < g;
-      const __nv_bfloat16* src = qrow + (8 * nt + r) * HD;
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int d = (u < 2 ? 16 * c + 8 * u : 64 + 16 * c + 8 * (u - 2));
-        raw[nt][u] = valid ? __ldg(reinterpret_cast<const uint4*>(src + d)) : make_uint4(0, 0, 0, 0);
-      }
-    }
     float amax = 0.0f;
 #pragma unroll
     for (int nt = 0; nt < NT; ++nt)

@@ -1,5 +1,5 @@
 #!/bin/bash
-# usage: scratch/prof_round.sh TAG  -- ncu captures of the decode kernel per config + launch list
+# usage: tools/prof_round.sh TAG  -- ncu captures of the decode kernel per config + launch list
 TAG=$1
 export KVQ_SKIP_NVCC=1
 for c in c2 c4 c3 c1; do

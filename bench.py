@@ -237,10 +237,19 @@ def run_ours(args, cfg):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world != args.gpus:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    # KVQ_BENCH_ONE_GPU=1 (debug only): run every rank on cuda:0 over gloo, to
+    # exercise the sharded code path on a single-GPU box.  Timings are then
+    # meaningless; the driver never sets it.
+    one_gpu = os.environ.get("KVQ_BENCH_ONE_GPU") == "1"
+    if one_gpu:
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if one_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
 
     from paper_2605_29639_b200 import KVCacheSpec, PagedKVCache, quantize_append
     from paper_2605_29639_b200.session import DecodeSession
@@ -397,7 +406,7 @@ def run_ours(args, cfg):
     achieved = attn_bytes / (k2_ms * 1e-3) / 1e9
     traffic = None
     tp = REPO / "profiles" / "ncu_traffic.json"
-    if tp.exists():
+    if tp.exists() and world == 1:  # the committed capture is a 1-GPU launch
         try:
             traffic = json.loads(tp.read_text()).get(args.config, {}).get("dram_bytes_per_launch")
         except Exception:

@@ -22,6 +22,8 @@
  *                         tiered_cache.py:355-363 (copy-on-write of a shared
  *                         partial tail block on fork).
  *   kvq_page_bytes     <- ClusterSim._block_bytes, simulator.py:178-179.
+ *   kvq_block_hashes   <- generate_hash_keys, blocks.py:51-69 (prefix-reuse
+ *                         identity of quantized pages).
  *
  * Error convention (mirrors the reference's ValueError / RuntimeError split,
  * errors.py:6-33): 0 = ok; KVQ_EINVAL (shape / dtype / alignment);
@@ -90,6 +92,14 @@ int kvq_decode_attn(const void* q, int64_t q_batch_stride, const void* pool, int
                     int32_t B, int32_t Hq, int32_t Hkv, int32_t kv_dtype, float sm_scale,
                     int32_t pages_per_split, void* workspace, size_t workspace_bytes, void* out,
                     int32_t out_dtype, int32_t out_layout, void* stream);
+
+/* Host-only.  Chained 64-bit keys of the complete `block_size`-token blocks
+ * of `tokens[0..n)` (FNV-1a over little-endian 8-byte words, chained from
+ * `prev_key`, or from the standard seed when 0): the prefix-reuse identity of
+ * quantized pages, same definition as the reference's block keys
+ * (blocks.py:29-69).  Returns the number of keys written, or KVQ_EINVAL. */
+int64_t kvq_block_hashes(const int64_t* tokens, int64_t n, int32_t block_size, uint64_t prev_key,
+                         uint64_t* out);
 
 /* Copy whole pages (all kv heads of a block): pairs[2*i] = src block,
  * pairs[2*i+1] = dst block (device int32). */

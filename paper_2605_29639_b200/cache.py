@@ -178,6 +178,8 @@ class BlockPool:
         self._heap: List[Tuple[int, int, object]] = []  # lazy (last_access, seq_no, key)
         self._by_block: Dict[int, object] = {}
         self._seq = 0
+        self._unref = 0          # resident entries with ref_count == 0 (evictable)
+        self.on_evict = None     # callable(key, block) before an evicted block is reused
         self.mutation_count = 0
 
     # -- introspection
@@ -187,6 +189,10 @@ class BlockPool:
     @property
     def num_free(self) -> int:
         return len(self._free)
+
+    @property
+    def num_evictable(self) -> int:
+        return self._unref
 
     def entry(self, key) -> Optional[BlockEntry]:
         return self._entries.get(key)
@@ -217,6 +223,7 @@ class BlockPool:
         self._seq += 1
         self._entries[key] = e
         self._by_block[blk] = key
+        self._unref += 1
         self.mutation_count += 1
         heapq.heappush(self._heap, (clock, e.seq_no, key))
         return blk
@@ -237,6 +244,8 @@ class BlockPool:
             if not self._heap:
                 raise CacheThrashError((nblocks - len(out)) * self.bytes_per_block)
             _, _, k = heapq.heappop(self._heap)
+            if self.on_evict is not None:
+                self.on_evict(k, self._entries[k].block)
             self.drop(k)
             out.append(k)
         return out
@@ -248,6 +257,7 @@ class BlockPool:
             raise ValueError("cannot drop a referenced block")
         self._free.append(e.block)
         del self._by_block[e.block]
+        self._unref -= 1
         self.mutation_count += 1
         return e.block
 
@@ -257,6 +267,8 @@ class BlockPool:
             raise KeyError(f"no entry for {key!r}")
         if self.is_partial(e) and e.ref_count >= 1:
             raise ValueError("partial block is exclusive")
+        if e.ref_count == 0:
+            self._unref -= 1
         e.ref_count += 1
         self._touch(e, clock)
         return e
@@ -267,6 +279,8 @@ class BlockPool:
             if e is None or e.ref_count <= 0:
                 raise ValueError("double release")
             e.ref_count -= 1
+            if e.ref_count == 0:
+                self._unref += 1
             self._touch(e, clock)
 
     def set_watermark(self, key, watermark: int) -> None:
@@ -302,6 +316,23 @@ class BlockPool:
 class _Seq:
     keys: List[object] = field(default_factory=list)
     length: int = 0
+    hashing: bool = False                  # token ids known: full pages get prefix keys
+    last_hash: int = 0                     # chain key of the last full page (0 = seed)
+    tail_tokens: List[int] = field(default_factory=list)
+
+
+def block_hashes(tokens: Sequence[int], block_size: int = BLOCK_SIZE, prev_key: int = 0) -> List[int]:
+    """Chained 64-bit keys of the complete pages of ``tokens`` (native
+    ``kvq_block_hashes``; the reference's block identity, ``blocks.py:51-69``)."""
+    from . import _lib
+    toks = np.ascontiguousarray(np.asarray(tokens, dtype=np.int64))
+    n = len(toks) // block_size
+    out = np.zeros(max(n, 1), dtype=np.uint64)
+    got = _lib.load().kvq_block_hashes(toks.ctypes.data if len(toks) else None, len(toks), block_size,
+                                       prev_key, out.ctypes.data)
+    if got < 0:
+        raise ValueError("kvq_block_hashes: bad arguments")
+    return [int(x) for x in out[:got]]
 
 
 class BlockAllocator:
@@ -360,19 +391,24 @@ class BlockAllocator:
         except KeyError:
             raise KeyError(f"unknown sequence {seq_id!r}") from None
 
+    @property
+    def num_available(self) -> int:
+        """Free blocks plus cached (unreferenced, evictable) prefix pages."""
+        return self.pool.num_free + self.pool.num_evictable
+
     def _new_block(self) -> object:
         key = ("anon", self._anon)
         self._anon += 1
-        if not self.pool.num_free:
+        if not self.num_available:
             raise CacheThrashError(self.bytes_per_block)
-        self.pool.insert(key, 0, self.clock)
+        self.pool.insert(key, 0, self.clock)  # evicts the LRU cached page when no block is free
         self.pool.acquire(key, self.clock)
         return key
 
     def _release(self, key) -> None:
         self.pool.release([key], self.clock)
-        if self.pool.entry(key).ref_count == 0:
-            self.pool.drop(key)
+        if self.pool.entry(key).ref_count == 0 and key[0] == "anon":
+            self.pool.drop(key)  # private page: free now; hashed full pages stay cached
 
     # -- sequence API
     def allocate(self, seq_id) -> None:
@@ -390,8 +426,8 @@ class BlockAllocator:
         bs = self.block_size
         tail_room = (bs - s.length % bs) % bs if s.keys else 0
         new_blocks = -(-(n - tail_room) // bs) if n > tail_room else 0
-        if new_blocks > self.pool.num_free:
-            raise CacheThrashError((new_blocks - self.pool.num_free) * self.bytes_per_block)
+        if new_blocks > self.num_available:
+            raise CacheThrashError((new_blocks - self.num_available) * self.bytes_per_block)
         self.clock += 1
         slots: List[int] = []
         pos = s.length
@@ -417,7 +453,7 @@ class BlockAllocator:
         self.clock += 1
         tail = p.keys[-1] if p.keys else None
         partial_tail = tail is not None and self.pool.is_partial(self.pool.entry(tail))
-        if partial_tail and not self.pool.num_free:
+        if partial_tail and not self.num_available:
             raise CacheThrashError(self.bytes_per_block)
         keys: List[object] = []
         for k in (p.keys[:-1] if partial_tail else p.keys):
@@ -429,8 +465,55 @@ class BlockAllocator:
             self.pool.set_watermark(dst, self.pool.entry(tail).watermark)
             keys.append(dst)
             copies.append((self.pool.lookup(tail), self.pool.lookup(dst)))
-        self._seqs[child_id] = _Seq(keys=keys, length=p.length)
+        self._seqs[child_id] = _Seq(keys=keys, length=p.length, hashing=p.hashing,
+                                    last_hash=p.last_hash, tail_tokens=list(p.tail_tokens))
         return copies
+
+    # -- prefix reuse (reference prefix identity blocks.py:51-69)
+    def allocate_prefix(self, seq_id, tokens: Sequence[int], promote=None) -> int:
+        """Register ``seq_id`` for prompt ``tokens`` and share the longest run
+        of leading full pages already resident under their chained keys
+        (``promote(key) -> bool`` may first bring a page back from a lower
+        tier).  Returns the number of prompt tokens covered; append the rest
+        with :meth:`append_tokens`."""
+        self.allocate(seq_id)
+        s = self._seqs[seq_id]
+        s.hashing = True
+        self.clock += 1
+        for h in block_hashes(tokens, self.block_size):
+            key = ("h", h)
+            if self.pool.entry(key) is None and not (promote is not None and promote(key)):
+                break
+            self.pool.acquire(key, self.clock)
+            s.keys.append(key)
+            s.length += self.block_size
+            s.last_hash = h
+        return s.length
+
+    def append_tokens(self, seq_id, tokens: Sequence[int]) -> List[int]:
+        """:meth:`append_slots` for known token ids: every page the tokens
+        complete is re-keyed to its chained prefix key, so later requests
+        with the same prefix can share it (it stays cached after free)."""
+        s = self._seq(seq_id)
+        if not s.hashing:
+            if s.length:
+                raise ValueError("sequence was filled without token ids")
+            s.hashing = True
+        first_page = s.length // self.block_size
+        slots = self.append_slots(seq_id, len(tokens))
+        pending = s.tail_tokens + [int(t) for t in tokens]
+        nfull = len(pending) // self.block_size
+        if nfull:
+            hashes = block_hashes(pending[: nfull * self.block_size], self.block_size, s.last_hash)
+            for i, h in enumerate(hashes):
+                page = first_page + i
+                old, new = s.keys[page], ("h", h)
+                if old[0] == "anon" and self.pool.entry(new) is None:
+                    self.pool.rekey(old, new)
+                    s.keys[page] = new
+            s.last_hash = hashes[-1]
+        s.tail_tokens = pending[nfull * self.block_size:]
+        return slots
 
     def free(self, seq_id) -> None:
         s = self._seqs.pop(seq_id, None)
@@ -465,8 +548,12 @@ class BlockAllocator:
                 wm = self.block_size if full else s.length - i * self.block_size
                 assert self.pool.entry(k).watermark == wm, "watermark mismatch"
         blocks = set()
+        unref = 0
         for k, e in self.pool._entries.items():
             assert e.ref_count == counts.get(k, 0), f"refcount mismatch on {k!r}"
+            if e.ref_count == 0:
+                unref += 1
+                assert k[0] == "h" and e.watermark == self.block_size, "only full hashed pages stay cached"
             assert e.block not in blocks, "physical block mapped twice"
             blocks.add(e.block)
             if e.watermark < self.block_size:
@@ -475,6 +562,7 @@ class BlockAllocator:
         assert len(free) == len(self.pool._free), "free list duplicates"
         assert not (free & blocks), "free block still mapped"
         assert len(free) + len(blocks) == self.num_blocks, "blocks lost"
+        assert unref == self.pool.num_evictable, "evictable counter"
 
 
 class BlockTable:

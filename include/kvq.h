@@ -101,6 +101,22 @@ int kvq_decode_attn(const void* q, int64_t q_batch_stride, const void* pool, int
 int64_t kvq_block_hashes(const int64_t* tokens, int64_t n, int32_t block_size, uint64_t prev_key,
                          uint64_t* out);
 
+/* Multi-query variant (speculative scoring / MTP): q_len query
+ * tokens per sequence, q: bf16 [B][q_len][Hq][128] (batch stride
+ * q_batch_stride, token stride Hq*128), causal within the q_len new tokens:
+ * query i sees seq_lens[b] - (q_len - 1 - i) tokens (seq_lens counts all of
+ * them).  out: [B*q_len][Hq][d] (KVQ_OUT_BHD) or [Hq][B*q_len][d].  Needs
+ * (Hq / Hkv) * q_len <= 16; size the workspace with
+ * kvq_decode_workspace_bytes(B, Hq * q_len, Hkv, max_splits).
+ * kvq_decode_attn is the q_len == 1 case.  Replaces the ScoreModel forward
+ * seam, spec_decode.py:98-107. */
+int kvq_decode_attn_mq(const void* q, int64_t q_batch_stride, int32_t q_len, const void* pool,
+                       int64_t num_blocks, const int32_t* block_table, int32_t max_blocks,
+                       const int32_t* seq_lens, int32_t B, int32_t Hq, int32_t Hkv, int32_t kv_dtype,
+                       float sm_scale, int32_t pages_per_split, void* workspace,
+                       size_t workspace_bytes, void* out, int32_t out_dtype, int32_t out_layout,
+                       void* stream);
+
 /* Copy whole pages (all kv heads of a block): pairs[2*i] = src block,
  * pairs[2*i+1] = dst block (device int32). */
 int kvq_copy_blocks(void* pool, int64_t num_blocks, int32_t Hkv, const int32_t* pairs,

@@ -34,6 +34,8 @@ SIGNATURES = {
     "kvq_decode_pages_per_split": (_i32, [_i32, _i32, _i64, _i32]),
     "kvq_decode_attn": (_c.c_int, [_vp, _i64, _vp, _i64, _vp, _i32, _vp, _i32, _i32, _i32, _i32,
                                    _f32, _i32, _vp, _sz, _vp, _i32, _i32, _vp]),
+    "kvq_decode_attn_mq": (_c.c_int, [_vp, _i64, _i32, _vp, _i64, _vp, _i32, _vp, _i32, _i32, _i32,
+                                      _i32, _f32, _i32, _vp, _sz, _vp, _i32, _i32, _vp]),
     "kvq_copy_blocks": (_c.c_int, [_vp, _i64, _i32, _vp, _i32, _vp]),
     "kvq_block_hashes": (_i64, [_vp, _i64, _i32, _c.c_uint64, _vp]),
 }
@@ -54,7 +56,8 @@ def load(path: Path | str | None = None) -> ctypes.CDLL:
     global _lib
     if _lib is not None and path is None:
         return _lib
-    p = Path(path) if path is not None else LIB_PATH
+    import os
+    p = Path(path) if path is not None else Path(os.environ.get("KVQ_LIB_PATH", LIB_PATH))
     if not p.exists():
         raise ImportError(
             f"{p} not found: build it with `python -c 'import __graft_entry__ as g; g.build()'` "

@@ -329,6 +329,8 @@ struct DecodeParams {
   int max_blocks;
   const int32_t* seq_lens;
   int B, Hq, Hkv, g;
+  int q_len;            // query tokens per sequence (1 = decode; k+1 = speculative scoring)
+  int G;                // query rows per kv head = g * q_len (<= 16)
   float sm_scale_log2;  // sm_scale * log2(e)
   int pages_per_split, max_splits;
   float* part_o;    // [B*Hq][max_splits][128]
@@ -356,10 +358,13 @@ struct Geo {
 };
 constexpr int CTAS_PER_SM = 4;  // used by the split heuristic (g <= 8 variant)
 
-__device__ __forceinline__ void store_out(const DecodeParams& p, int b, int head, int d0,
+// Query row j of kv head h (j < G) is query token i = j / g of head h*g + j % g.
+// Output rows are query tokens t = b * q_len + i: [T][Hq][d] or head-major [Hq][T][d].
+__device__ __forceinline__ void store_out(const DecodeParams& p, int b, int h, int j, int d0,
                                           const float* vals) {
-  // 8 contiguous values starting at d0 for (b, head).
-  const int64_t row = p.out_hbd ? ((int64_t)head * p.B + b) : ((int64_t)b * p.Hq + head);
+  const int i = j / p.g, head = h * p.g + j % p.g;
+  const int64_t t = (int64_t)b * p.q_len + i;
+  const int64_t row = p.out_hbd ? ((int64_t)head * p.B * p.q_len + t) : (t * p.Hq + head);
   if (p.out_f32) {
     float* o = reinterpret_cast<float*>(p.out) + row * HD + d0;
     *reinterpret_cast<float4*>(o) = make_float4(vals[0], vals[1], vals[2], vals[3]);
@@ -437,7 +442,7 @@ struct PageStream {
 // movmatrix transpose per 8x8 block.  d is permuted inside each k-step /
 // m-tile so every thread reads 16-byte chunks (bank-conflict-free given the
 // page swizzle).
-template <int KVD, bool HI>
+template <int KVD, bool HI, bool MQ>
 __global__ void __launch_bounds__(THREADS, Geo<HI>::CTAS) decode_kernel(const DecodeParams p) {
   constexpr int NT = Geo<HI>::NT;
   constexpr int S = Geo<HI>::S;
@@ -447,7 +452,8 @@ __global__ void __launch_bounds__(THREADS, Geo<HI>::CTAS) decode_kernel(const De
   uint2* qsm = reinterpret_cast<uint2*>(smem + NW * S * PAGE + NW * S * sizeof(uint64_t) + 16);
 
   const int split = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
-  const int g = p.g;
+  // MQ: q_len > 1 query tokens per sequence (compile-time off for plain decode).
+  const int g = p.g, G = MQ ? p.G : p.g, qlen = MQ ? p.q_len : 1;
   const int L = min(__ldg(p.seq_lens + b), p.max_blocks * BS);
   const int npages = (L + BS - 1) / BS;
   const int nsplit = max(1, (npages + p.pages_per_split - 1) / p.pages_per_split);
@@ -456,8 +462,8 @@ __global__ void __launch_bounds__(THREADS, Geo<HI>::CTAS) decode_kernel(const De
 
   if (L <= 0) {  // empty sequence: zeros, nothing to combine
     const float z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    for (int idx = threadIdx.x; idx < g * (HD / 8); idx += THREADS)
-      store_out(p, b, h * g + idx / (HD / 8), (idx % (HD / 8)) * 8, z);
+    for (int idx = threadIdx.x; idx < G * (HD / 8); idx += THREADS)
+      store_out(p, b, h, idx / (HD / 8), (idx % (HD / 8)) * 8, z);
     return;
   }
   const int pg0 = split * p.pages_per_split;
@@ -467,11 +473,13 @@ __global__ void __launch_bounds__(THREADS, Geo<HI>::CTAS) decode_kernel(const De
   uint4 raw[NT][4];
   {
     const int r = lane >> 2, c = lane & 3;
-    const __nv_bfloat16* qrow = p.q + (int64_t)b * p.q_stride_b + (int64_t)(h * g) * HD;
+    const __nv_bfloat16* qb = p.q + (int64_t)b * p.q_stride_b;
 #pragma unroll
     for (int nt = 0; nt < NT; ++nt) {
-      const bool valid = 8 * nt + r < g;
-      const __nv_bfloat16* src = qrow + (8 * nt + r) * HD;
+      const int j = 8 * nt + r;  // query row: token j / g, head h*g + j % g
+      const bool valid = j < G;
+      const __nv_bfloat16* src = MQ ? qb + ((int64_t)(j / g) * p.Hq + h * g + j % g) * HD
+                                    : qb + (int64_t)(h * g + j) * HD;
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         const int d = (u < 2 ? 16 * c + 8 * u : 64 + 16 * c + 8 * (u - 2));
@@ -616,10 +624,14 @@ __global__ void __launch_bounds__(THREADS, Geo<HI>::CTAS) decode_kernel(const De
     for (int e = 0; e < 2; ++e) {
       m[nt][e] = -INFINITY;
       l[nt][e] = 0.0f;
-      hvalid[nt][e] = 8 * nt + 2 * c + e < g;
+      hvalid[nt][e] = 8 * nt + 2 * c + e < G;
     }
   float escale = 1.0f;  // V-scale normaliser 2^E (fp16 range guard for P')
   bool escale_set = false;
+  // Causal visibility of query row j (token i = j / g of q_len): L - (q_len - 1 - i);
+  // only evaluated on tail pages, so it costs no registers in the steady state.
+  const int L_all = L - (qlen - 1);  // tokens visible to every query row
+  auto vis = [&](int nt, int e) { return MQ ? L_all + (8 * nt + 2 * c + e) / g : L; };
 
   int slot = 0;
   uint32_t phase = 0;
@@ -716,7 +728,7 @@ __global__ void __launch_bounds__(THREADS, Geo<HI>::CTAS) decode_kernel(const De
     // ---- scores relative to the running max, log2 units: u = S^T * scale_k * qscale - m
     //      (one FFMA); thread holds tokens r, r+8 x heads 2c, 2c+1 per n-tile.
     const int tok_base = (pg0 + warp + j * NW) * BS;
-    const bool tail = tok_base + BS > L;
+    const bool tail = tok_base + BS > L_all;  // page holds tokens some query row must not see
     const bool ok_r = !tail || tok_base + r < L, ok_r8 = !tail || tok_base + r + 8 < L;
     if (!ok_r) vs_r = 0.0f;
     if (!ok_r8) vs_r8 = 0.0f;
@@ -728,7 +740,7 @@ __global__ void __launch_bounds__(THREADS, Geo<HI>::CTAS) decode_kernel(const De
     for (int nt = 0; nt < NT; ++nt) {
 #pragma unroll
       for (int q4 = 0; q4 < 4; ++q4) {
-        const bool ok = q4 < 2 ? ok_r : ok_r8;
+        const bool ok = !tail || tok_base + (q4 < 2 ? r : r + 8) < vis(nt, q4 & 1);
         u[nt][q4] = ok ? fmaf(st[nt][q4], q4 < 2 ? kq_r : kq_r8, -m[nt][q4 & 1]) : -INFINITY;
         over |= hvalid[nt][q4 & 1] && u[nt][q4] > 8.0f;
       }
@@ -747,7 +759,8 @@ __global__ void __launch_bounds__(THREADS, Geo<HI>::CTAS) decode_kernel(const De
       for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
         for (int e = 0; e < 2; ++e)
-          mx[nt][e] = fmaxf(ok_r ? st[nt][e] * kq_r : -INFINITY, ok_r8 ? st[nt][e + 2] * kq_r8 : -INFINITY);
+          mx[nt][e] = fmaxf((!tail || tok_base + r < vis(nt, e)) ? st[nt][e] * kq_r : -INFINITY,
+                            (!tail || tok_base + r + 8 < vis(nt, e)) ? st[nt][e + 2] * kq_r8 : -INFINITY);
       float vmax = fmaxf(vs_r, vs_r8);
 #pragma unroll
       for (int o2 = 4; o2 <= 16; o2 <<= 1) {
@@ -788,7 +801,7 @@ __global__ void __launch_bounds__(THREADS, Geo<HI>::CTAS) decode_kernel(const De
         }
 #pragma unroll
         for (int q4 = 0; q4 < 4; ++q4) {
-          const bool ok = q4 < 2 ? ok_r : ok_r8;
+          const bool ok = !tail || tok_base + (q4 < 2 ? r : r + 8) < vis(nt, q4 & 1);
           u[nt][q4] = ok ? fmaf(st[nt][q4], q4 < 2 ? kq_r : kq_r8, -m[nt][q4 & 1]) : -INFINITY;
         }
       }
@@ -889,7 +902,7 @@ __global__ void __launch_bounds__(THREADS, Geo<HI>::CTAS) decode_kernel(const De
   __syncthreads();
   // Each thread finalises 8 contiguous d of one head row.
   const int tid = threadIdx.x;
-  const int nrow_items = g * (HD / 8);
+  const int nrow_items = G * (HD / 8);
   for (int item = tid; item < nrow_items; item += THREADS) {
     const int row = item / (HD / 8), d0 = (item % (HD / 8)) * 8;
     float M = -INFINITY;
@@ -909,14 +922,14 @@ __global__ void __launch_bounds__(THREADS, Geo<HI>::CTAS) decode_kernel(const De
     const float inv = 1.0f / lsum;
 #pragma unroll
     for (int e = 0; e < 8; ++e) acc[e] *= inv;
-    const int head = h * g + row;
+    const int64_t vrow = ((int64_t)b * p.Hkv + h) * G + row;  // partial row of (b, h, query row)
     if (nsplit == 1) {
-      store_out(p, b, head, d0, acc);
+      store_out(p, b, h, row, d0, acc);
     } else {
-      float* dst = p.part_o + (((int64_t)b * p.Hq + head) * p.max_splits + split) * HD + d0;
+      float* dst = p.part_o + (vrow * p.max_splits + split) * HD + d0;
       *reinterpret_cast<float4*>(dst) = make_float4(acc[0], acc[1], acc[2], acc[3]);
       *reinterpret_cast<float4*>(dst + 4) = make_float4(acc[4], acc[5], acc[6], acc[7]);
-      if (d0 == 0) p.part_lse[((int64_t)b * p.Hq + head) * p.max_splits + split] = M + __log2f(lsum);
+      if (d0 == 0) p.part_lse[vrow * p.max_splits + split] = M + __log2f(lsum);
     }
   }
   if (nsplit == 1) return;
@@ -939,8 +952,7 @@ __global__ void __launch_bounds__(THREADS, Geo<HI>::CTAS) decode_kernel(const De
   if (!*flag) return;
   for (int item = tid; item < nrow_items; item += THREADS) {
     const int row = item / (HD / 8), d0 = (item % (HD / 8)) * 8;
-    const int head = h * g + row;
-    const int64_t base = ((int64_t)b * p.Hq + head) * p.max_splits;
+    const int64_t base = (((int64_t)b * p.Hkv + h) * G + row) * p.max_splits;
     float M = -INFINITY;
 #pragma unroll 4
     for (int sp = 0; sp < nsplit; ++sp) M = fmaxf(M, __ldcg(p.part_lse + base + sp));
@@ -963,7 +975,7 @@ __global__ void __launch_bounds__(THREADS, Geo<HI>::CTAS) decode_kernel(const De
     const float inv = 1.0f / wsum;
 #pragma unroll
     for (int e = 0; e < 8; ++e) acc[e] *= inv;
-    store_out(p, b, head, d0, acc);
+    store_out(p, b, h, row, d0, acc);
   }
 }
 
@@ -1092,16 +1104,17 @@ int32_t kvq_decode_pages_per_split(int32_t B, int32_t Hkv, int64_t total_pages, 
   return (int32_t)(pps > 0 ? pps : 1);
 }
 
-int kvq_decode_attn(const void* q, int64_t q_batch_stride, const void* pool, int64_t num_blocks,
-                    const int32_t* block_table, int32_t max_blocks, const int32_t* seq_lens,
-                    int32_t B, int32_t Hq, int32_t Hkv, int32_t kv_dtype, float sm_scale,
-                    int32_t pages_per_split, void* workspace, size_t workspace_bytes, void* out,
-                    int32_t out_dtype, int32_t out_layout, void* stream) {
-  if (B < 0 || Hq <= 0 || Hkv <= 0 || max_blocks <= 0 || num_blocks <= 0)
+int kvq_decode_attn_mq(const void* q, int64_t q_batch_stride, int32_t q_len, const void* pool,
+                       int64_t num_blocks, const int32_t* block_table, int32_t max_blocks,
+                       const int32_t* seq_lens, int32_t B, int32_t Hq, int32_t Hkv, int32_t kv_dtype,
+                       float sm_scale, int32_t pages_per_split, void* workspace,
+                       size_t workspace_bytes, void* out, int32_t out_dtype, int32_t out_layout,
+                       void* stream) {
+  if (B < 0 || Hq <= 0 || Hkv <= 0 || max_blocks <= 0 || num_blocks <= 0 || q_len <= 0)
     return fail(KVQ_EINVAL, "decode_attn: bad sizes");
   if (B == 0) return KVQ_OK;
-  if (Hq % Hkv != 0 || Hq / Hkv > 16)
-    return fail(KVQ_EINVAL, "decode_attn: need Hq % Hkv == 0 and Hq / Hkv <= 16");
+  if (Hq % Hkv != 0 || (Hq / Hkv) * q_len > 16)
+    return fail(KVQ_EINVAL, "decode_attn: need Hq % Hkv == 0 and (Hq / Hkv) * q_len <= 16");
   if (!q || !pool || !block_table || !seq_lens || !out || !workspace)
     return fail(KVQ_EINVAL, "decode_attn: null pointer");
   if (!aligned(q, 16) || (q_batch_stride % 8) || !aligned(pool, 16) || !aligned(out, 16) ||
@@ -1116,7 +1129,8 @@ int kvq_decode_attn(const void* q, int64_t q_batch_stride, const void* pool, int
   if (pages_per_split <= 0)
     pages_per_split = kvq_decode_pages_per_split(B, Hkv, (int64_t)B * max_blocks, max_blocks);
   const int max_splits = (max_blocks + pages_per_split - 1) / pages_per_split;
-  if (workspace_bytes < kvq_decode_workspace_bytes(B, Hq, Hkv, max_splits))
+  const int64_t rows = (int64_t)Hq * q_len;  // query rows per sequence
+  if (workspace_bytes < kvq_decode_workspace_bytes(B, (int32_t)rows, Hkv, max_splits))
     return fail(KVQ_EINVAL, "decode_attn: workspace too small");
   if (int rc = check_device()) return rc;
 
@@ -1134,20 +1148,22 @@ int kvq_decode_attn(const void* q, int64_t q_batch_stride, const void* pool, int
   prm.Hq = Hq;
   prm.Hkv = Hkv;
   prm.g = Hq / Hkv;
+  prm.q_len = q_len;
+  prm.G = prm.g * q_len;
   prm.sm_scale_log2 = sm_scale * 1.4426950408889634f;
   prm.pages_per_split = pages_per_split;
   prm.max_splits = max_splits;
   prm.counters = reinterpret_cast<int*>(ws);
   prm.part_o = reinterpret_cast<float*>(ws + up((size_t)B * Hkv * sizeof(int)));
   prm.part_lse = reinterpret_cast<float*>(ws + up((size_t)B * Hkv * sizeof(int)) +
-                                          up((size_t)B * Hq * max_splits * KVQ_HEAD_DIM * sizeof(float)));
+                                          up((size_t)B * rows * max_splits * KVQ_HEAD_DIM * sizeof(float)));
   prm.out = out;
   prm.out_f32 = out_dtype == KVQ_OUT_F32;
   prm.out_hbd = out_layout == KVQ_OUT_HBD;
 
   const dim3 grid((unsigned)max_splits, (unsigned)Hkv, (unsigned)B);
   auto st = static_cast<cudaStream_t>(stream);
-  const bool hi = prm.g > 8;
+  const bool hi = prm.G > 8;
   const size_t smem_bytes = hi ? kvq::Geo<true>::SMEM : kvq::Geo<false>::SMEM;
   auto launch = [&](auto kernel) -> int {
     cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1159,10 +1175,26 @@ int kvq_decode_attn(const void* q, int64_t q_batch_stride, const void* pool, int
     kernel<<<grid, kvq::THREADS, smem_bytes, st>>>(prm);
     return check_launch("decode_attn");
   };
-  if (kv_dtype == KVQ_INT8)
-    return hi ? launch(kvq::decode_kernel<KVQ_INT8, true>) : launch(kvq::decode_kernel<KVQ_INT8, false>);
-  return hi ? launch(kvq::decode_kernel<KVQ_FP8_E4M3, true>)
-            : launch(kvq::decode_kernel<KVQ_FP8_E4M3, false>);
+  const bool mq = q_len > 1;
+  if (kv_dtype == KVQ_INT8) {
+    if (mq) return hi ? launch(kvq::decode_kernel<KVQ_INT8, true, true>) : launch(kvq::decode_kernel<KVQ_INT8, false, true>);
+    return hi ? launch(kvq::decode_kernel<KVQ_INT8, true, false>) : launch(kvq::decode_kernel<KVQ_INT8, false, false>);
+  }
+  if (mq)
+    return hi ? launch(kvq::decode_kernel<KVQ_FP8_E4M3, true, true>)
+              : launch(kvq::decode_kernel<KVQ_FP8_E4M3, false, true>);
+  return hi ? launch(kvq::decode_kernel<KVQ_FP8_E4M3, true, false>)
+            : launch(kvq::decode_kernel<KVQ_FP8_E4M3, false, false>);
+}
+
+int kvq_decode_attn(const void* q, int64_t q_batch_stride, const void* pool, int64_t num_blocks,
+                    const int32_t* block_table, int32_t max_blocks, const int32_t* seq_lens,
+                    int32_t B, int32_t Hq, int32_t Hkv, int32_t kv_dtype, float sm_scale,
+                    int32_t pages_per_split, void* workspace, size_t workspace_bytes, void* out,
+                    int32_t out_dtype, int32_t out_layout, void* stream) {
+  return kvq_decode_attn_mq(q, q_batch_stride, 1, pool, num_blocks, block_table, max_blocks, seq_lens,
+                            B, Hq, Hkv, kv_dtype, sm_scale, pages_per_split, workspace, workspace_bytes,
+                            out, out_dtype, out_layout, stream);
 }
 
 int kvq_copy_blocks(void* pool, int64_t num_blocks, int32_t Hkv, const int32_t* pairs,

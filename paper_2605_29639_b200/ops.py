@@ -90,7 +90,10 @@ def paged_decode_attention(q: torch.Tensor, cache: PagedKVCache, block_table: to
                            out_dtype: torch.dtype = torch.bfloat16, head_major: bool = False,
                            workspace: Optional[torch.Tensor] = None) -> torch.Tensor:
     """GQA decode attention of one query token per sequence over the paged,
-    quantized KV cache.
+    quantized KV cache -- or, with ``q`` of shape ``[B, q_len, Hq, 128]``, of
+    ``q_len`` new tokens per sequence (speculative scoring / MTP), causal
+    among them: token i sees ``seq_lens[b] - (q_len - 1 - i)`` tokens, so
+    ``seq_lens`` counts all of them (they must already be appended).
 
     q: bf16 ``[B, Hq, 128]``; block_table: int32 ``[B, max_blocks]``;
     seq_lens: int32 ``[B]``.  Returns ``[B, Hq, 128]`` (or ``[Hq, B, 128]``
@@ -99,11 +102,13 @@ def paged_decode_attention(q: torch.Tensor, cache: PagedKVCache, block_table: to
     pages, when the host knows it) sharpens the split-KV geometry."""
     _require_cuda("paged_decode_attention", q, block_table, seq_lens, cache.pool)
     spec = cache.spec
-    if q.dtype != torch.bfloat16 or q.dim() != 3 or q.shape[2] != 128 or q.stride(2) != 1:
-        raise ValueError("paged_decode_attention: q must be bf16 [B, Hq, 128]")
-    B, Hq = q.shape[0], q.shape[1]
-    if q.stride(1) != 128:
-        raise ValueError("paged_decode_attention: q heads must be contiguous")
+    multi = q.dim() == 4  # [B, q_len, Hq, 128]: speculative scoring / MTP (causal among the new tokens)
+    if q.dtype != torch.bfloat16 or q.dim() not in (3, 4) or q.shape[-1] != 128 or q.stride(-1) != 1:
+        raise ValueError("paged_decode_attention: q must be bf16 [B, Hq, 128] or [B, q_len, Hq, 128]")
+    B, Hq = q.shape[0], q.shape[-2]
+    q_len = q.shape[1] if multi else 1
+    if q.stride(-2) != 128 or (multi and q.stride(1) != Hq * 128):
+        raise ValueError("paged_decode_attention: q heads (and query tokens) must be contiguous")
     if block_table.dtype != torch.int32 or block_table.dim() != 2 or block_table.shape[0] != B \
             or not block_table.is_contiguous():
         raise ValueError("paged_decode_attention: block_table must be contiguous int32 [B, max_blocks]")
@@ -112,7 +117,10 @@ def paged_decode_attention(q: torch.Tensor, cache: PagedKVCache, block_table: to
     if out_dtype not in (torch.bfloat16, torch.float32):
         raise ValueError("paged_decode_attention: out_dtype must be bf16 or fp32")
     max_blocks = block_table.shape[1]
-    shape = (Hq, B, 128) if head_major else (B, Hq, 128)
+    if head_major:
+        shape = (Hq, B * q_len, 128)
+    else:
+        shape = (B, q_len, Hq, 128) if multi else (B, Hq, 128)
     if out is None:
         out = torch.empty(shape, dtype=out_dtype, device=q.device)
     elif tuple(out.shape) != shape or out.dtype != out_dtype or not out.is_contiguous():
@@ -125,15 +133,15 @@ def paged_decode_attention(q: torch.Tensor, cache: PagedKVCache, block_table: to
     pps = pages_per_split or lib.kvq_decode_pages_per_split(
         B, spec.num_kv_heads, total_pages if total_pages is not None else B * max_blocks, max_blocks)
     max_splits = -(-max_blocks // pps)
-    nbytes = lib.kvq_decode_workspace_bytes(B, Hq, spec.num_kv_heads, max_splits)
+    nbytes = lib.kvq_decode_workspace_bytes(B, Hq * q_len, spec.num_kv_heads, max_splits)
     if workspace is None:
         workspace = _workspace(q.device, nbytes, ((B * spec.num_kv_heads * 4 + 255) // 256) * 256)
     elif workspace.numel() * workspace.element_size() < nbytes:
         raise ValueError(f"paged_decode_attention: workspace needs {nbytes} bytes")
-    st = lib.kvq_decode_attn(
-        q.data_ptr(), q.stride(0), cache.pool.data_ptr(), cache.num_blocks, block_table.data_ptr(),
-        max_blocks, seq_lens.data_ptr(), B, Hq, spec.num_kv_heads, spec.kv_dtype_id,
-        float(sm_scale), int(pps), workspace.data_ptr(),
+    st = lib.kvq_decode_attn_mq(
+        q.data_ptr(), q.stride(0), q_len, cache.pool.data_ptr(), cache.num_blocks,
+        block_table.data_ptr(), max_blocks, seq_lens.data_ptr(), B, Hq, spec.num_kv_heads,
+        spec.kv_dtype_id, float(sm_scale), int(pps), workspace.data_ptr(),
         workspace.numel() * workspace.element_size(), out.data_ptr(),
         _lib.KVQ_OUT_F32 if out_dtype == torch.float32 else _lib.KVQ_OUT_BF16,
         _lib.KVQ_OUT_HBD if head_major else _lib.KVQ_OUT_BHD, _stream_handle(q.device))

@@ -125,3 +125,30 @@ def test_split_combine_is_race_free(cuda, pps):
         ws[cnt:].fill_(0x7F if trial % 2 else 0xFF)
         again = paged_decode_attention(*args, out_dtype=torch.float32, pages_per_split=pps, workspace=ws)
         assert torch.equal(again, base), f"trial {trial}"
+
+
+@pytest.mark.parametrize("kv_dtype", [O.INT8, O.FP8_E4M3])
+@pytest.mark.parametrize("q_len,Hq,Hkv", [(4, 32, 8), (2, 64, 8), (3, 16, 4), (1, 32, 8), (16, 8, 8)])
+def test_multi_query_causal(cuda, kv_dtype, q_len, Hq, Hkv):
+    """q_len draft tokens per sequence, causal among themselves.
+    Oracle: query i of sequence b == single-query attention over the first
+    seq_len - (q_len - 1 - i) tokens."""
+    lens = [700, 16 + q_len, 1300, 33]
+    sc = Scenario(lens, Hq, Hkv, kv_dtype, seed=50 + q_len)
+    g = torch.Generator().manual_seed(9)
+    q4 = torch.randn((sc.B, q_len, Hq, 128), generator=g).to(torch.bfloat16)
+    cache = PagedKVCache(KVCacheSpec(Hkv, kv_dtype=NAMES[kv_dtype]), sc.num_blocks, device=cuda,
+                         pool=torch.from_numpy(sc.pool).to(cuda))
+    out = paged_decode_attention(q4.to(cuda), cache, torch.from_numpy(sc.block_table).to(cuda),
+                                 torch.from_numpy(sc.seq_lens).to(cuda), out_dtype=torch.float32,
+                                 pages_per_split=7).cpu().numpy()
+    # expanded single-query batch for the oracle
+    qe = q4.reshape(sc.B * q_len, Hq, 128)
+    table = np.repeat(sc.block_table, q_len, axis=0)
+    le = np.asarray([L - (q_len - 1 - i) for L in sc.seq_lens for i in range(q_len)], np.int32)
+    ref = O.decode_attn(bf16_bits(qe), sc.pool, table, le, Hkv, kv_dtype).reshape(sc.B, q_len, Hq, 128)
+    assert rel_err(out, ref) <= 2e-3
+    hm = paged_decode_attention(q4.to(cuda), cache, torch.from_numpy(sc.block_table).to(cuda),
+                                torch.from_numpy(sc.seq_lens).to(cuda), out_dtype=torch.float32,
+                                pages_per_split=7, head_major=True).cpu().numpy()
+    assert np.array_equal(hm.transpose(1, 0, 2).reshape(sc.B, q_len, Hq, 128), out)

@@ -324,33 +324,82 @@ def run_ours(args, cfg):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
-    # ---- device-resident timed region: CUDA-graph replays of K1 and K2 ------
+    # ---- device-resident timed region: one CUDA graph of all K steps ---------
+    # Each step is [K1, event, K2, event (, all-gather)]; the graph holds the W
+    # warm-up steps or the K timed steps unrolled, so there is no per-step host
+    # launch in the timed region.  The K2 events are graph event-record nodes.
     sess._kernels(buf)  # warm the kernels (and lazy module loading) before capture
+    if world > 1:
+        gather_dev(buf["out"])  # communicator set up before any capture
     torch.cuda.synchronize()
-    g_append, g_attn = sess.capture()
+    gather_in_graph = world > 1 and not one_gpu
 
-    def step(ev=None):
-        g_append.replay()
-        if ev is not None:
-            ev[0].record()
-        g_attn.replay()
-        if ev is not None:
-            ev[1].record()
-        if world > 1:
+    # Event-record nodes cost a few microseconds of launch bubble each, so
+    # only every k2_every-th step brackets its K2 (the per-launch sample).
+    k2_every = max(1, args.k2_sample_every)
+
+    def capture_steps(n, timed):
+        evs = {}
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            for i in range(n):
+                sess.k1(buf)
+                if timed and i % k2_every == 0:
+                    evs[i] = (torch.cuda.Event(enable_timing=True, external=True),
+                              torch.cuda.Event(enable_timing=True, external=True))
+                    evs[i][0].record()
+                sess.k2(buf)
+                if i in evs:
+                    evs[i][1].record()
+                if gather_in_graph:
+                    gather_dev(buf["out"])
+        return g, list(evs.values())
+
+    graphs = None
+    if world == 1 or gather_in_graph:
+        try:
+            graphs = capture_steps(args.warmup, False)[0], capture_steps(args.steps, True)
+        except Exception as e:  # e.g. a NCCL build that cannot be captured: eager gather
+            print(f"[bench] step capture with the all-gather failed ({e}); eager gather", file=sys.stderr)
+            torch.cuda.synchronize()
+    if graphs is not None:
+        g_warm, (g_timed, evs) = graphs
+
+        def run_warm():
+            g_warm.replay()
+
+        def run_timed():
+            g_timed.replay()
+    else:  # gloo debug mode (or no NCCL capture): per-step graphs of K1 and K2, eager gather
+        g_append, g_attn = sess.capture()
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+               for _ in range(args.steps)]
+
+        def one(ev=None):
+            g_append.replay()
+            if ev is not None:
+                ev[0].record()
+            g_attn.replay()
+            if ev is not None:
+                ev[1].record()
             gather_dev(buf["out"])
 
-    for _ in range(args.warmup):
-        step()
+        def run_warm():
+            for _ in range(args.warmup):
+                one()
+
+        def run_timed():
+            for i in range(args.steps):
+                one(evs[i])
+
+    run_warm()
     barrier()
-    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-           for _ in range(args.steps)]
     t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     sampler = ClockSampler(local)
     barrier()
     with sampler:
         t_start.record()
-        for i in range(args.steps):
-            step(evs[i])
+        run_timed()
         t_end.record()
         torch.cuda.synchronize()
     ms_total = max_over_ranks(t_start.elapsed_time(t_end))
@@ -425,7 +474,8 @@ def run_ours(args, cfg):
                    "l2": "inputs larger than L2 (pool %.2f GB vs 126 MB L2); no flush" % (cache.nbytes() * world / 1e9)
                    if cache.nbytes() * world > 4 * 126e6 else "pool fits in L2: L2-resident numbers",
                    "step": "K1 append of B rows + K2 paged decode attention (+ all-gather if N>1); "
-                           "stationary ctx; device steps replay CUDA graphs of K1 and K2",
+                           "stationary ctx; the K timed steps are one CUDA graph (K1, K2 per step, unrolled); "
+                           "K2 launch time from event nodes around every k2_sample_every-th K2",
                    "e2e": "DecodeSession.submit: H2D of q/k/v/slots/lens from pinned memory, K1, K2, "
                           "(all-gather), D2H of O; double-buffered copy streams overlap adjacent steps",
                    "compute": "TMA bulk page copies; QK^T: INT8 codes on s8 tensor cores (mma m16n8k32, two-term int8 Q) / E4M3 codes -> f16 (mma m16n8k16); PV: codes -> f16, mma m16n8k16 f32 accumulate"},
@@ -433,6 +483,7 @@ def run_ours(args, cfg):
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "kernel": "kvq::decode_kernel",
                      "algorithmic_bytes_per_launch": attn_bytes, "avg_launch_ms": k2_ms,
+                     "launches_sampled": len(evs),
                      "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)" if peak_kind == "measured"
                      else "fallback 6.65 TB/s (B200_PROFILING.md)"},
         "e2e": {"value": B / (e2e_ms * 1e-3), "unit": "tokens/s", "h2d_bytes_per_step": h2d,
@@ -602,6 +653,8 @@ def main(argv=None):
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--k2-sample-every", type=int, default=8,
+                    help="bracket every n-th step's K2 with CUDA events (the per-launch roofline sample)")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--pages-per-split", type=int, default=None,
                     help="override the split-KV geometry (default: kvq_decode_pages_per_split)")

@@ -204,6 +204,78 @@ __global__ void __launch_bounds__(K1_THREADS) quant_append_kernel(
 }
 
 // ---------------------------------------------------------------------------
+// K1r: the decode-shaped append (a few tokens, each in a different page).
+// One warp per (token, head): lane l quantizes K and V elements [4l, 4l+4)
+// (one LDG.64 each), so the per-warp chain is ~100 instructions and a
+// B = 256 x 8-head step spreads over 256 CTAs instead of 32.  Same rounding
+// as quantize16 (the amax is an exact max, independent of the lane split).
+// ---------------------------------------------------------------------------
+constexpr int K1R_WARPS = 8;
+// Up to this many (token, head) rows a launch takes the one-warp-per-row kernel.
+constexpr int64_t K1_ROWS_MAX = 8192;
+
+template <int KVD>
+__device__ __forceinline__ uint32_t codes4(const float (&x)[4], float inv) {
+  float y[4];
+#pragma unroll
+  for (int e = 0; e < 4; ++e) y[e] = __fmul_rn(x[e], inv);
+  if constexpr (KVD == KVQ_FP8_E4M3) {
+    uint16_t l, h;
+    asm("cvt.rn.satfinite.e4m3x2.f32 %0, %1, %2;" : "=h"(l) : "f"(y[1]), "f"(y[0]));
+    asm("cvt.rn.satfinite.e4m3x2.f32 %0, %1, %2;" : "=h"(h) : "f"(y[3]), "f"(y[2]));
+    return (uint32_t)l | ((uint32_t)h << 16);
+  } else {
+    uint32_t word = 0;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int c = max(-127, min(127, __float2int_rn(y[e])));  // NaN -> 0, saturating
+      word |= ((uint32_t)(c & 0xff)) << (8 * e);
+    }
+    return word;
+  }
+}
+
+template <int KVD>
+__global__ void __launch_bounds__(K1R_WARPS * 32) quant_append_rows_kernel(
+    const __nv_bfloat16* __restrict__ k, const __nv_bfloat16* __restrict__ v, int64_t k_stride,
+    int64_t v_stride, const int32_t* __restrict__ slots, int T, int Hkv,
+    uint8_t* __restrict__ pool, int64_t num_blocks) {
+  const int row = blockIdx.x * K1R_WARPS + (threadIdx.x >> 5);  // t * Hkv + h
+  const int lane = threadIdx.x & 31;
+  if (row >= T * Hkv) return;  // whole warps only
+  const int t = row / Hkv, h = row - t * Hkv;
+  const uint2 kw = __ldg(reinterpret_cast<const uint2*>(k + (int64_t)t * k_stride + h * HD + 4 * lane));
+  const uint2 vw = __ldg(reinterpret_cast<const uint2*>(v + (int64_t)t * v_stride + h * HD + 4 * lane));
+  const int slot = __ldg(slots + t);
+  float xk[4], xv[4];
+  xk[0] = __uint_as_float(kw.x << 16), xk[1] = __uint_as_float(kw.x & 0xffff0000u);
+  xk[2] = __uint_as_float(kw.y << 16), xk[3] = __uint_as_float(kw.y & 0xffff0000u);
+  xv[0] = __uint_as_float(vw.x << 16), xv[1] = __uint_as_float(vw.x & 0xffff0000u);
+  xv[2] = __uint_as_float(vw.y << 16), xv[3] = __uint_as_float(vw.y & 0xffff0000u);
+  float ak = fmaxf(fmaxf(fabsf(xk[0]), fabsf(xk[1])), fmaxf(fabsf(xk[2]), fabsf(xk[3])));
+  float av = fmaxf(fmaxf(fabsf(xv[0]), fabsf(xv[1])), fmaxf(fabsf(xv[2]), fabsf(xv[3])));
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    ak = fmaxf(ak, __shfl_xor_sync(FULL, ak, o));
+    av = fmaxf(av, __shfl_xor_sync(FULL, av, o));
+  }
+  if (slot < 0 || (slot >> 4) >= num_blocks) return;
+  const float qmax = KVD == KVQ_FP8_E4M3 ? 448.0f : 127.0f;
+  const float ik = ak > 0.0f ? __fdiv_rn(qmax, ak) : 0.0f;
+  const float iv = av > 0.0f ? __fdiv_rn(qmax, av) : 0.0f;
+  const uint32_t ck = codes4<KVD>(xk, ik), cv = codes4<KVD>(xv, iv);
+  const int tok = slot & 15;
+  uint8_t* page = pool + ((int64_t)(slot >> 4) * Hkv + h) * PAGE;
+  *reinterpret_cast<uint32_t*>(page + k_code_off(tok, 4 * lane)) = ck;
+#pragma unroll
+  for (int e = 0; e < 4; ++e) page[v_code_off(tok, 4 * lane + e)] = (uint8_t)(cv >> (8 * e));
+  if (lane < 2) {
+    const float a = lane ? av : ak;
+    *reinterpret_cast<float*>(page + (lane ? VS_OFF : KS_OFF) + 4 * tok) = __fdiv_rn(a, qmax);
+  }
+}
+
+// ---------------------------------------------------------------------------
 // PTX helpers: shared-memory addresses, mbarriers, bulk async copy, MMA.
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -1043,28 +1115,41 @@ int kvq_quant_append(const void* k, const void* v, int64_t k_token_stride, int64
     return fail(KVQ_EUNSUPPORTED, "quant_append: unknown kv dtype");
   if (int rc = check_device()) return rc;
   if (Hkv > 65535) return fail(KVQ_EINVAL, "quant_append: Hkv too large");
-  const dim3 grid((unsigned)((T + 15) / 16), (unsigned)((Hkv + kvq::K1_HEADS - 1) / kvq::K1_HEADS));
   auto st = static_cast<cudaStream_t>(stream);
   // Same (max-shared) L1/smem carveout as K2 so a decode step never pays an
   // SM reconfiguration between the append and the attention kernel.
   static const bool carve = [] {
-    cudaFuncSetAttribute(kvq::quant_append_kernel<KVQ_INT8>, cudaFuncAttributePreferredSharedMemoryCarveout,
-                         cudaSharedmemCarveoutMaxShared);
-    cudaFuncSetAttribute(kvq::quant_append_kernel<KVQ_FP8_E4M3>,
-                         cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
-    cudaFuncSetAttribute(kvq::copy_blocks_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
-                         cudaSharedmemCarveoutMaxShared);
+    const void* fns[] = {(const void*)kvq::quant_append_kernel<KVQ_INT8>,
+                         (const void*)kvq::quant_append_kernel<KVQ_FP8_E4M3>,
+                         (const void*)kvq::quant_append_rows_kernel<KVQ_INT8>,
+                         (const void*)kvq::quant_append_rows_kernel<KVQ_FP8_E4M3>,
+                         (const void*)kvq::copy_blocks_kernel};
+    for (const void* f : fns)
+      cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
     return true;
   }();
   (void)carve;
+  const auto kp = static_cast<const __nv_bfloat16*>(k);
+  const auto vp = static_cast<const __nv_bfloat16*>(v);
+  auto* pp = static_cast<uint8_t*>(pool);
+  if ((int64_t)T * Hkv <= kvq::K1_ROWS_MAX) {
+    // Decode-shaped batch: latency-bound, one warp per (token, head).
+    const unsigned nblk = (unsigned)((T * Hkv + kvq::K1R_WARPS - 1) / kvq::K1R_WARPS);
+    if (kv_dtype == KVQ_INT8)
+      kvq::quant_append_rows_kernel<KVQ_INT8><<<nblk, kvq::K1R_WARPS * 32, 0, st>>>(
+          kp, vp, k_token_stride, v_token_stride, slot_mapping, T, Hkv, pp, num_blocks);
+    else
+      kvq::quant_append_rows_kernel<KVQ_FP8_E4M3><<<nblk, kvq::K1R_WARPS * 32, 0, st>>>(
+          kp, vp, k_token_stride, v_token_stride, slot_mapping, T, Hkv, pp, num_blocks);
+    return check_launch("quant_append");
+  }
+  const dim3 grid((unsigned)((T + 15) / 16), (unsigned)((Hkv + kvq::K1_HEADS - 1) / kvq::K1_HEADS));
   if (kv_dtype == KVQ_INT8)
     kvq::quant_append_kernel<KVQ_INT8><<<grid, kvq::K1_THREADS, 0, st>>>(
-        static_cast<const __nv_bfloat16*>(k), static_cast<const __nv_bfloat16*>(v), k_token_stride,
-        v_token_stride, slot_mapping, T, Hkv, static_cast<uint8_t*>(pool), num_blocks);
+        kp, vp, k_token_stride, v_token_stride, slot_mapping, T, Hkv, pp, num_blocks);
   else
     kvq::quant_append_kernel<KVQ_FP8_E4M3><<<grid, kvq::K1_THREADS, 0, st>>>(
-        static_cast<const __nv_bfloat16*>(k), static_cast<const __nv_bfloat16*>(v), k_token_stride,
-        v_token_stride, slot_mapping, T, Hkv, static_cast<uint8_t*>(pool), num_blocks);
+        kp, vp, k_token_stride, v_token_stride, slot_mapping, T, Hkv, pp, num_blocks);
   return check_launch("quant_append");
 }
 

@@ -71,12 +71,21 @@ class DecodeSession:
                 gather=gather_factory() if self.sharded else None, used=False))
         self.step_idx = 0
 
-    def _kernels(self, buf) -> None:
+    def k1(self, buf) -> None:
+        """Quantize-on-append of the step's new K/V rows (device buffers)."""
         quantize_append(self.cache, buf["k"], buf["v"], buf["slots"])
+
+    def k2(self, buf) -> None:
+        """Paged decode attention over the cache into ``buf["out"]``."""
         paged_decode_attention(buf["q"], self.cache, self.block_table, buf["lens"], out=buf["out"],
                                head_major=self.head_major, sm_scale=self.sm_scale,
                                pages_per_split=self.pps, out_dtype=self.out_dtype,
                                workspace=buf["ws"])
+
+    def _kernels(self, buf, k1: bool = True) -> None:
+        if k1:
+            self.k1(buf)
+        self.k2(buf)
 
     def submit(self, q_h: torch.Tensor, k_h: torch.Tensor, v_h: torch.Tensor, slots_h: torch.Tensor,
                lens_h: torch.Tensor, out_h: torch.Tensor) -> torch.cuda.Event:
@@ -115,11 +124,7 @@ class DecodeSession:
         """CUDA graphs [K1, K2] of one step over device buffer 0's contents."""
         buf = self.bufs[0]
         graphs = []
-        for fn in (lambda: quantize_append(self.cache, buf["k"], buf["v"], buf["slots"]),
-                   lambda: paged_decode_attention(
-                       buf["q"], self.cache, self.block_table, buf["lens"], out=buf["out"],
-                       head_major=self.head_major, sm_scale=self.sm_scale, pages_per_split=self.pps,
-                       out_dtype=self.out_dtype, workspace=buf["ws"])):
+        for fn in (lambda: self.k1(buf), lambda: self.k2(buf)):
             g = torch.cuda.CUDAGraph()
             with torch.cuda.graph(g):
                 fn()

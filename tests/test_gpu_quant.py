@@ -13,7 +13,22 @@ pytestmark = pytest.mark.gpu
 DT = {"int8": O.INT8, "fp8_e4m3": O.FP8_E4M3}
 
 
-def run_both(k, v, slots, Hkv, kv_dtype, num_blocks, cuda):
+# Launches of up to K1_ROWS_MAX (token, head) rows take the one-warp-per-row
+# kernel, larger ones the 16-token tile kernel.  ``tile=True`` pads the call
+# with skipped (-1) slots so the same content also runs through the tile kernel.
+K1_ROWS_MAX = 8192
+
+
+def pad_to_tile(k, v, slots, Hkv):
+    extra = K1_ROWS_MAX // Hkv + 1
+    z = torch.zeros((extra, Hkv, 128), dtype=k.dtype)
+    return (torch.cat([k, z]), torch.cat([v, z]),
+            np.concatenate([np.asarray(slots, np.int32), np.full(extra, -1, np.int32)]))
+
+
+def run_both(k, v, slots, Hkv, kv_dtype, num_blocks, cuda, tile=False):
+    if tile:
+        k, v, slots = pad_to_tile(k, v, slots, Hkv)
     cache = PagedKVCache(KVCacheSpec(Hkv, kv_dtype=kv_dtype), num_blocks, device=cuda)
     quantize_append(cache, k.to(cuda), v.to(cuda), torch.as_tensor(slots, dtype=torch.int32, device=cuda))
     gpu = cache.pool.cpu().numpy()
@@ -23,7 +38,7 @@ def run_both(k, v, slots, Hkv, kv_dtype, num_blocks, cuda):
 
 
 @pytest.mark.parametrize("kv_dtype", ["int8", "fp8_e4m3"])
-@pytest.mark.parametrize("T,Hkv", [(1, 8), (37, 4), (256, 8), (2048, 8), (300, 1)])
+@pytest.mark.parametrize("T,Hkv", [(1, 8), (37, 4), (256, 8), (1024, 8), (1025, 8), (2048, 8), (300, 1)])
 def test_append_bit_exact(cuda, kv_dtype, T, Hkv):
     num_blocks = (T + 15) // 16 + 5
     rng = np.random.default_rng(T * 7 + Hkv)
@@ -55,15 +70,16 @@ def edge_rows():
     return np.stack(rows)
 
 
+@pytest.mark.parametrize("tile", [False, True])
 @pytest.mark.parametrize("kv_dtype", ["int8", "fp8_e4m3"])
-def test_append_edge_cases(cuda, kv_dtype):
+def test_append_edge_cases(cuda, kv_dtype, tile):
     x = edge_rows()
     T = x.shape[0]
     bits = O.f32_to_bf16_bits(x)
     k = torch.from_numpy(bits.view(np.int16)).view(torch.bfloat16).reshape(T, 1, 128)
     v = torch.from_numpy(bits[::-1].copy().view(np.int16)).view(torch.bfloat16).reshape(T, 1, 128)
     slots = np.arange(T, dtype=np.int32)
-    gpu, ref = run_both(k, v, slots, 1, kv_dtype, (T + 15) // 16, cuda)
+    gpu, ref = run_both(k, v, slots, 1, kv_dtype, (T + 15) // 16, cuda, tile=tile)
     diff = np.nonzero(gpu != ref)
     assert diff[0].size == 0, f"mismatch at {list(zip(*diff))[:8]}: gpu {gpu[diff][:8]} ref {ref[diff][:8]}"
 
@@ -84,8 +100,9 @@ def test_append_strided_and_skipped(cuda):
     assert not ref[0].any(), "block 0 must stay untouched"
 
 
+@pytest.mark.parametrize("tile", [False, True])
 @pytest.mark.parametrize("kv_dtype", ["int8", "fp8_e4m3"])
-def test_append_whole_pages_and_mixed(cuda, kv_dtype):
+def test_append_whole_pages_and_mixed(cuda, kv_dtype, tile):
     """Chunked-prefill shape: runs of 16 block-aligned slots take the
     whole-page path; a misaligned run and scattered decode slots in the same
     call take the per-row path.  Bytes must match the oracle either way."""
@@ -98,5 +115,5 @@ def test_append_whole_pages_and_mixed(cuda, kv_dtype):
     slots = np.asarray(slots, dtype=np.int32)
     T = len(slots)
     k, v = make_kv(T, Hkv, 31, kind="k"), make_kv(T, Hkv, 32, kind="v")
-    gpu, ref = run_both(k, v, slots, Hkv, kv_dtype, num_blocks, cuda)
+    gpu, ref = run_both(k, v, slots, Hkv, kv_dtype, num_blocks, cuda, tile=tile)
     assert np.array_equal(gpu, ref), f"{(gpu != ref).sum()} bytes differ"

@@ -33,12 +33,17 @@ class DecodeSession:
     def __init__(self, cache: PagedKVCache, block_table: torch.Tensor, batch: int, num_q_heads: int,
                  *, total_pages: Optional[int] = None, out_dtype: torch.dtype = torch.bfloat16,
                  head_major: bool = False, sm_scale: Optional[float] = None, depth: int = 2,
-                 gather_factory=None, pages_per_split: Optional[int] = None):
+                 gather_factory=None, pages_per_split: Optional[int] = None, graphs: bool = False):
         """With ``gather_factory`` (returning a
         :class:`paper_2605_29639_b200.shard.OutputGather`, one per buffer slot,
         for KV-head / 2-D sharding) the local head-major output
         ``[Hq_loc, B_r, d]`` is assembled into ``[Hq, B, d]`` on the compute
-        stream before the download."""
+        stream before the download.
+
+        With ``graphs=True`` each buffer slot's device work (K1, K2 and the
+        gather) is captured once as a CUDA graph on first use and replayed by
+        every later :meth:`submit`: one host call per step instead of one
+        per kernel."""
         dev = cache.device
         self.sharded = gather_factory is not None
         if self.sharded:
@@ -56,20 +61,39 @@ class DecodeSession:
         self.h2d = torch.cuda.Stream(dev)
         self.d2h = torch.cuda.Stream(dev)
         oshape = (num_q_heads, batch, 128) if head_major else (batch, num_q_heads, 128)
+        # The step's inputs live in one packed blob per slot (q | k | v | slots |
+        # lens, 16-byte aligned), mirrored by a pinned host staging blob, so a
+        # staged step uploads with a single copy.
+        shapes = (("q", (batch, num_q_heads, 128), torch.bfloat16), ("k", (batch, self.Hkv, 128), torch.bfloat16),
+                  ("v", (batch, self.Hkv, 128), torch.bfloat16), ("slots", (batch,), torch.int32),
+                  ("lens", (batch,), torch.int32))
+        layout, off = [], 0
+        for name, shape, dt in shapes:
+            n = 1
+            for x in shape:
+                n *= x
+            nbytes = n * torch.empty((), dtype=dt).element_size()
+            layout.append((name, shape, dt, off, nbytes))
+            off = (off + nbytes + 15) & ~15
+        self.in_bytes = off
+        pin = torch.cuda.is_available()
+
+        def views(blob):
+            return {name: blob[o: o + nb].view(dt).view(shape) for name, shape, dt, o, nb in layout}
+
         self.bufs = []
         for _ in range(depth):
+            dev_in = torch.empty(max(off, 16), dtype=torch.uint8, device=dev)
+            host_in = torch.empty(max(off, 16), dtype=torch.uint8, pin_memory=pin)
             self.bufs.append(dict(
-                q=torch.empty((batch, num_q_heads, 128), dtype=torch.bfloat16, device=dev),
-                k=torch.empty((batch, self.Hkv, 128), dtype=torch.bfloat16, device=dev),
-                v=torch.empty((batch, self.Hkv, 128), dtype=torch.bfloat16, device=dev),
-                slots=torch.empty((batch,), dtype=torch.int32, device=dev),
-                lens=torch.empty((batch,), dtype=torch.int32, device=dev),
+                **views(dev_in), dev_in=dev_in, host_in=host_in, host=views(host_in),
                 out=torch.empty(oshape, dtype=out_dtype, device=dev),
                 ws=torch.zeros(workspace_bytes(batch, num_q_heads, self.Hkv, max_splits),
                                dtype=torch.uint8, device=dev),
                 in_ready=torch.cuda.Event(), done=torch.cuda.Event(), out_done=torch.cuda.Event(),
                 gather=gather_factory() if self.sharded else None, used=False))
         self.step_idx = 0
+        self.graphs = graphs
 
     def k1(self, buf) -> None:
         """Quantize-on-append of the step's new K/V rows (device buffers)."""
@@ -91,23 +115,25 @@ class DecodeSession:
                lens_h: torch.Tensor, out_h: torch.Tensor) -> torch.cuda.Event:
         """Enqueue one decode step.  Host tensors should be pinned; they must
         stay untouched until the returned event completes."""
+        return self._submit((q_h, k_h, v_h, slots_h, lens_h), out_h)
+
+    def _submit(self, inputs, out_h: torch.Tensor) -> torch.cuda.Event:
         buf = self.bufs[self.step_idx % self.depth]
         self.step_idx += 1
         with torch.cuda.stream(self.h2d):
             if buf["used"]:
                 self.h2d.wait_event(buf["done"])      # previous kernels finished reading
-            buf["q"].copy_(q_h, non_blocking=True)
-            buf["k"].copy_(k_h, non_blocking=True)
-            buf["v"].copy_(v_h, non_blocking=True)
-            buf["slots"].copy_(slots_h, non_blocking=True)
-            buf["lens"].copy_(lens_h, non_blocking=True)
+            if inputs is None:
+                buf["dev_in"].copy_(buf["host_in"], non_blocking=True)
+            else:
+                for name, t in zip(("q", "k", "v", "slots", "lens"), inputs):
+                    buf[name].copy_(t, non_blocking=True)
             buf["in_ready"].record(self.h2d)
         self.compute.wait_event(buf["in_ready"])
         if buf["used"]:
             self.compute.wait_event(buf["out_done"])   # previous download of this out buffer
         with torch.cuda.stream(self.compute):
-            self._kernels(buf)
-            full = buf["gather"](buf["out"]) if self.sharded else buf["out"]
+            full = self._device_step(buf)
         buf["done"].record(self.compute)
         with torch.cuda.stream(self.d2h):
             self.d2h.wait_event(buf["done"])
@@ -115,6 +141,38 @@ class DecodeSession:
             buf["out_done"].record(self.d2h)
         buf["used"] = True
         return buf["out_done"]
+
+    def next_inputs(self) -> dict:
+        """Pinned host views ``{q, k, v, slots, lens}`` of the staging blob the
+        next :meth:`submit_staged` uploads.  Waits (host side) until that
+        slot's previous upload has finished, so the views may be overwritten."""
+        buf = self.bufs[self.step_idx % self.depth]
+        if buf["used"]:
+            buf["in_ready"].synchronize()
+        return buf["host"]
+
+    def submit_staged(self, out_h: torch.Tensor) -> torch.cuda.Event:
+        """Enqueue one step whose inputs were written into :meth:`next_inputs`:
+        one host-to-device copy, the device step, one device-to-host copy."""
+        return self._submit(None, out_h)
+
+    def _device_step(self, buf) -> torch.Tensor:
+        if not self.graphs:
+            self._kernels(buf)
+            return buf["gather"](buf["out"]) if self.sharded else buf["out"]
+        g = buf.get("graph")
+        if g is None:
+            # Warm once eagerly (module load, NCCL communicator), then capture.
+            self._kernels(buf)
+            full = buf["gather"](buf["out"]) if self.sharded else buf["out"]
+            self.compute.synchronize()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=torch.cuda.Stream(self.cache.device)):
+                self._kernels(buf)
+                full = buf["gather"](buf["out"]) if self.sharded else buf["out"]
+            buf["graph"], buf["graph_out"] = g, full
+        buf["graph"].replay()
+        return buf["graph_out"]
 
     def synchronize(self) -> None:
         for s in (self.h2d, self.compute, self.d2h):

@@ -84,3 +84,43 @@ def test_session_back_to_back_and_graphs(cuda):
     g2.replay()
     torch.cuda.synchronize()
     assert torch.equal(buf["out"].cpu(), outs[0])
+
+
+@pytest.mark.parametrize("staged", [False, True])
+def test_session_graphs_and_staged_match_eager(cuda, staged):
+    """graphs=True (one captured graph per buffer slot) and the single-copy
+    staged upload give the eager session's bytes, step after step, while the
+    steps' inputs change."""
+    sc = Scenario([200, 33, 900, 17, 64], 32, 8, O.INT8, seed=23, extra_blocks=4)
+    table = torch.from_numpy(sc.block_table).to(cuda)
+    pool0 = torch.from_numpy(sc.pool).to(cuda)
+    caches = [PagedKVCache(KVCacheSpec(8), sc.num_blocks, device=cuda, pool=pool0.clone()) for _ in range(2)]
+    eager = DecodeSession(caches[0], table, sc.B, 32)
+    fast = DecodeSession(caches[1], table, sc.B, 32, graphs=True)
+    g = torch.Generator().manual_seed(9)
+    lens = torch.from_numpy(sc.seq_lens)
+    # re-append the last token of each sequence with new values each step
+    slots = torch.tensor([int(sc.block_table[b, (L - 1) // 16]) * 16 + (L - 1) % 16
+                          for b, L in enumerate(sc.seq_lens)], dtype=torch.int32)
+    outs = []
+    for step in range(7):
+        q = torch.randn((sc.B, 32, 128), generator=g).to(torch.bfloat16)
+        k = torch.randn((sc.B, 8, 128), generator=g).to(torch.bfloat16)
+        v = torch.randn((sc.B, 8, 128), generator=g).to(torch.bfloat16)
+        o_a = torch.empty((sc.B, 32, 128), dtype=torch.bfloat16, pin_memory=True)
+        o_b = torch.empty_like(o_a).pin_memory()
+        eager.submit(q.pin_memory(), k.pin_memory(), v.pin_memory(), slots.pin_memory(), lens.pin_memory(), o_a)
+        if staged:
+            h = fast.next_inputs()
+            for name, t in (("q", q), ("k", k), ("v", v), ("slots", slots), ("lens", lens)):
+                h[name].copy_(t)
+            fast.submit_staged(o_b)
+        else:
+            fast.submit(q.pin_memory(), k.pin_memory(), v.pin_memory(), slots.pin_memory(), lens.pin_memory(), o_b)
+        outs.append((o_a, o_b))
+        eager.synchronize()   # the two sessions share nothing but keep their pools in lock step
+        fast.synchronize()
+    for a, b in outs:
+        assert torch.equal(a, b)
+    assert torch.equal(caches[0].pool, caches[1].pool)
+    assert len({int(o[0].float().sum()) for o in outs}) > 1, "inputs must change between steps"

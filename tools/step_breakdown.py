@@ -101,6 +101,27 @@ def main():
     for name, g in gu.items():
         t = timed(g.replay, max(1, args.iters // U))
         res[f"{name} x{U} unrolled"] = (t[0] / U,) + t[1:]
+    # End to end through DecodeSession.submit (pinned host buffers), eager vs graphs.
+    q_h = buf["q"].cpu().pin_memory()
+    k_h, v_h = buf["k"].cpu().pin_memory(), buf["v"].cpu().pin_memory()
+    s_h, l_h = buf["slots"].cpu().pin_memory(), buf["lens"].cpu().pin_memory()
+    o_h = torch.empty((Hq, B, 128), dtype=torch.bfloat16, pin_memory=True)
+    for graphs in (False, True):
+        se = DecodeSession(cache, table_d, B, Hq, total_pages=nb, head_major=True, graphs=graphs)
+
+        def e2e():
+            se.submit(q_h, k_h, v_h, s_h, l_h, o_h)
+        for _ in range(5):
+            e2e()
+        se.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(se.h2d)
+        n = args.iters
+        for _ in range(n):
+            e2e()
+        e1.record(se.d2h)
+        se.synchronize()
+        res[f"e2e graphs={graphs}"] = (e0.elapsed_time(e1) / n * 1e3, None, "")
     print(args.config, f"pps={sess.pps}", " | ".join(f"{k} {v[0]:.2f} us @{v[1]} {v[2]}" for k, v in res.items()), flush=True)
 
 

@@ -253,7 +253,7 @@ def run_ours(args, cfg):
 
     from paper_2605_29639_b200 import KVCacheSpec, PagedKVCache, quantize_append
     from paper_2605_29639_b200.session import DecodeSession
-    from paper_2605_29639_b200.shard import OutputGather, plan_shards
+    from paper_2605_29639_b200.shard import OutputGather, PeerOutput, plan_shards
 
     B, Hq, Hkv = cfg["B"], cfg["Hq"], cfg["Hkv"]
     lens_all = ctx_lens(cfg)
@@ -304,13 +304,24 @@ def run_ours(args, cfg):
     def make_gather():
         return OutputGather(plan, Hq, B, torch.bfloat16, dev)
 
+    # N > 1: the all-gather is fused into K2 (peer-memory stores + flags) unless
+    # --gather nccl asks for the separate NCCL collective (the baseline).
+    peer = None
+    gather_mode = "none" if world == 1 else args.gather
+    if gather_mode == "peer":
+        try:
+            peer = PeerOutput(plan, Hq, B, Hkv, dev, slots=2)
+        except Exception as e:  # setup-time capability check (e.g. no CUDA IPC): fall back to NCCL
+            print(f"[bench] fused peer gather unavailable ({e}); NCCL all-gather", file=sys.stderr)
+            gather_mode = f"nccl (peer setup failed: {type(e).__name__})"
+    use_nccl = world > 1 and peer is None
     sess = DecodeSession(cache, table_d, B_loc, Hq_loc, total_pages=total_pages, head_major=True,
-                         gather_factory=make_gather if world > 1 else None,
+                         gather_factory=make_gather if use_nccl else None, peer=peer,
                          pages_per_split=args.pages_per_split)
     buf = sess.device_buffers(0)
     for name, t in (("q", q), ("k", k_new), ("v", v_new), ("slots", slots_step), ("lens", seq_lens_d)):
         buf[name].copy_(t)
-    gather_dev = make_gather() if world > 1 else None
+    gather_dev = make_gather() if use_nccl else None
 
     def barrier():
         if world > 1:
@@ -329,10 +340,10 @@ def run_ours(args, cfg):
     # warm-up steps or the K timed steps unrolled, so there is no per-step host
     # launch in the timed region.  The K2 events are graph event-record nodes.
     sess._kernels(buf)  # warm the kernels (and lazy module loading) before capture
-    if world > 1:
+    if use_nccl:
         gather_dev(buf["out"])  # communicator set up before any capture
     torch.cuda.synchronize()
-    gather_in_graph = world > 1 and not one_gpu
+    gather_in_graph = use_nccl and not one_gpu
 
     # Event-record nodes cost a few microseconds of launch bubble each, so
     # only every k2_every-th step brackets its K2 (the per-launch sample).
@@ -356,7 +367,7 @@ def run_ours(args, cfg):
         return g, list(evs.values())
 
     graphs = None
-    if world == 1 or gather_in_graph:
+    if not use_nccl or gather_in_graph:
         try:
             graphs = capture_steps(args.warmup, False)[0], capture_steps(args.steps, True)
         except Exception as e:  # e.g. a NCCL build that cannot be captured: eager gather
@@ -382,7 +393,8 @@ def run_ours(args, cfg):
             g_attn.replay()
             if ev is not None:
                 ev[1].record()
-            gather_dev(buf["out"])
+            if gather_dev is not None:
+                gather_dev(buf["out"])
 
         def run_warm():
             for _ in range(args.warmup):
@@ -413,8 +425,8 @@ def run_ours(args, cfg):
     # D2H copy of O.  The stationary inputs are written into both slots'
     # staging blobs once; every step still uploads them.
     es = DecodeSession(cache, table_d, B_loc, Hq_loc, total_pages=total_pages, head_major=True,
-                       gather_factory=make_gather if world > 1 else None,
-                       pages_per_split=args.pages_per_split, graphs=not one_gpu)
+                       gather_factory=make_gather if use_nccl else None, peer=peer,
+                       pages_per_split=args.pages_per_split, graphs=not (one_gpu and use_nccl))
     host_inputs = {"q": q, "k": k_new, "v": v_new, "slots": slots_step, "lens": seq_lens_d}
     for b in es.bufs:
         for name, t in host_inputs.items():
@@ -453,10 +465,15 @@ def run_ours(args, cfg):
         cpu = {"value": sample.B / dt, "unit": "tokens/s", "cores": sample.threads, "kind": "port",
                "sample": sample.describe() + f"; {reps} reps, {dt * 1e3:.1f} ms/step"}
 
+    peer_errors = peer.errors() if peer is not None else 0
+    if peer is not None:
+        peer.close()
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()
         return
+    if peer_errors:
+        raise SystemExit(f"fused peer gather: {peer_errors} slot(s) timed out")
     attn_bytes, append_bytes = algorithmic_bytes(lens, Hq_loc, Hkv_loc, B_loc)
     peak, peak_kind = measured_peak()
     achieved = attn_bytes / (k2_ms * 1e-3) / 1e9
@@ -475,6 +492,9 @@ def run_ours(args, cfg):
         "dtype": cfg["kv"].replace("fp8_e4m3", "e4m3"), "data": "synthetic",
         "config": {"workload": cfg["workload"], "name": args.config, "global_batch": B,
                    "sum_ctx": int((lens_all + 1).sum()),
+                   "gather": {"none": "none (1 GPU)",
+                              "peer": "fused into K2: peer-memory row stores + done/free flags (no collective launch)",
+                              "nccl": "NCCL all_gather_into_tensor after K2"}.get(gather_mode, gather_mode),
                    "parallelism": (f"kv-head tp{world}" if plan.b_split == 1 else
                                    f"{plan.h_split} kv-head groups x {plan.b_split} LPT batch parts")
                    if world > 1 else "1 GPU",
@@ -666,6 +686,9 @@ def main(argv=None):
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--pages-per-split", type=int, default=None,
                     help="override the split-KV geometry (default: kvq_decode_pages_per_split)")
+    ap.add_argument("--gather", default="peer", choices=["peer", "nccl"],
+                    help="N > 1: fuse the KV-head output all-gather into K2 over peer memory (default) "
+                         "or run NCCL all_gather_into_tensor after K2")
     ap.add_argument("--kv", default=None, choices=["int8", "fp8_e4m3"],
                     help="override the config's KV dtype (the C5 INT8 vs FP8 sweep)")
     args = ap.parse_args(argv)

@@ -122,6 +122,54 @@ int kvq_decode_attn_mq(const void* q, int64_t q_batch_stride, int32_t q_len, con
 int kvq_copy_blocks(void* pool, int64_t num_blocks, int32_t Hkv, const int32_t* pairs,
                     int32_t n_pairs, void* stream);
 
+/* ---- KV-head sharding with the output all-gather fused into K2 ----------
+ * Replaces the separate all-gather of the sharded decode (the
+ * reference models TP only as cost parameters).  Every
+ * rank owns one "symmetric" buffer per output slot: a control block
+ * (KVQ_PEER_CTL_BYTES) followed by the global bf16 output [Hq][B][128].
+ * Each rank maps every peer's buffer (CUDA IPC over NVLink / NVSwitch), and
+ * its K2 writes each finished output row straight into all P copies, then
+ * bumps a "done" counter in every peer's control block.  The last CTA of the
+ * grid waits until all P ranks' rows of this use have landed, so when K2
+ * completes on a rank, its global output is complete: no collective launch,
+ * and the transfer overlaps the attention tile by tile.  Slot reuse is safe:
+ * K2 releases the slot's previous use at start (stream order guarantees that
+ * use was consumed), and a writer waits for every rank's release before
+ * overwriting.  All protocol state lives in device memory, so the launch is
+ * CUDA-graph capturable.  Spins time out after ~10 s and set the error word
+ * of the local control block instead of hanging. */
+#define KVQ_MAX_PEERS 8
+#define KVQ_PEER_CTL_BYTES 256 /* uint32 words: [0] done [1] uses [2] error [3] arrivals [32+i] free[i] */
+#define KVQ_IPC_HANDLE_BYTES 64
+typedef struct kvq_peer_out {
+  int32_t n_peers;          /* P, 2..KVQ_MAX_PEERS */
+  int32_t rank;             /* this rank's index in out[] / ctl[] */
+  int32_t head_offset;      /* first global q head this rank computes */
+  int32_t batch_global;     /* B of the global [Hq][B][128] output */
+  const int32_t* seq_map;   /* device int32 [B_local]: local sequence -> global row (NULL = identity) */
+  uint32_t writers_per_use; /* sum over ranks of B_r * Hkv_r: done increments per use */
+  uint32_t reserved;
+  void* out[KVQ_MAX_PEERS]; /* rank i's global output of this slot (mapped into this process) */
+  void* ctl[KVQ_MAX_PEERS]; /* rank i's control block of this slot */
+} kvq_peer_out;
+
+/* kvq_decode_attn with the gather fused: same arguments, but the output goes
+ * to peer->out[0..P) (bf16, [Hq_global][batch_global][128], rows of heads
+ * head_offset .. head_offset + Hq) instead of an `out` pointer.  q_len == 1. */
+int kvq_decode_attn_peer(const void* q, int64_t q_batch_stride, const void* pool, int64_t num_blocks,
+                         const int32_t* block_table, int32_t max_blocks, const int32_t* seq_lens,
+                         int32_t B, int32_t Hq, int32_t Hkv, int32_t kv_dtype, float sm_scale,
+                         int32_t pages_per_split, void* workspace, size_t workspace_bytes,
+                         const kvq_peer_out* peer, void* stream);
+
+/* Symmetric-buffer plumbing (setup time only, not on the step path):
+ * allocate `bytes` of zeroed device memory on the current device and return
+ * its IPC handle; map a peer's handle into this process; unmap; free. */
+int kvq_sym_alloc(size_t bytes, void** ptr, void* ipc_handle);
+int kvq_sym_open(const void* ipc_handle, void** ptr);
+int kvq_sym_close(void* ptr);
+int kvq_sym_free(void* ptr);
+
 #ifdef __cplusplus
 }
 #endif

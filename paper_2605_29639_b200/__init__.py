@@ -8,10 +8,11 @@ ABI of ``libkvq.so`` (include/kvq.h).
 """
 from .cache import (BlockAllocator, BlockTable, CacheThrashError, KVCacheSpec, PagedKVCache,
                     unpack_pages)
-from .ops import copy_blocks, paged_decode_attention, quantize_append
+from .ops import copy_blocks, paged_decode_attention, paged_decode_attention_gathered, quantize_append
 
 __all__ = [
     "BlockAllocator", "BlockTable", "CacheThrashError", "KVCacheSpec", "PagedKVCache",
-    "unpack_pages", "copy_blocks", "paged_decode_attention", "quantize_append",
+    "unpack_pages", "copy_blocks", "paged_decode_attention", "paged_decode_attention_gathered",
+    "quantize_append",
 ]
 __version__ = "0.1.0"

@@ -38,7 +38,24 @@ SIGNATURES = {
                                       _i32, _f32, _i32, _vp, _sz, _vp, _i32, _i32, _vp]),
     "kvq_copy_blocks": (_c.c_int, [_vp, _i64, _i32, _vp, _i32, _vp]),
     "kvq_block_hashes": (_i64, [_vp, _i64, _i32, _c.c_uint64, _vp]),
+    "kvq_decode_attn_peer": (_c.c_int, [_vp, _i64, _vp, _i64, _vp, _i32, _vp, _i32, _i32, _i32, _i32,
+                                        _f32, _i32, _vp, _sz, _vp, _vp]),
+    "kvq_sym_alloc": (_c.c_int, [_sz, _c.POINTER(_vp), _vp]),
+    "kvq_sym_open": (_c.c_int, [_vp, _c.POINTER(_vp)]),
+    "kvq_sym_close": (_c.c_int, [_vp]),
+    "kvq_sym_free": (_c.c_int, [_vp]),
 }
+
+MAX_PEERS = 8
+PEER_CTL_BYTES = 256
+IPC_HANDLE_BYTES = 64
+
+
+class PeerOutDesc(_c.Structure):
+    """``kvq_peer_out`` (include/kvq.h): one output slot of the fused gather."""
+    _fields_ = [("n_peers", _i32), ("rank", _i32), ("head_offset", _i32), ("batch_global", _i32),
+                ("seq_map", _vp), ("writers_per_use", _c.c_uint32), ("reserved", _c.c_uint32),
+                ("out", _vp * MAX_PEERS), ("ctl", _vp * MAX_PEERS)]
 
 _lib = None
 

@@ -19,6 +19,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdio.h>
+#include <string.h>
 
 #include "kvq.h"
 
@@ -410,6 +411,7 @@ struct DecodeParams {
   int* counters;    // [B*Hkv]
   void* out;
   int out_f32, out_hbd;
+  kvq_peer_out peer;    // n_peers == 0: local output only (no fused gather)
 };
 
 constexpr int NW = 4;  // warps per CTA; every warp streams its own pages
@@ -430,11 +432,109 @@ struct Geo {
 };
 constexpr int CTAS_PER_SM = 4;  // used by the split heuristic (g <= 8 variant)
 
+__device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
+  __nv_bfloat162 t = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<uint32_t*>(&t);
+}
+
+// ---------------------------------------------------------------------------
+// Fused KV-head gather over peer memory (kvq_peer_out, include/kvq.h).
+// Control block words (uint32) of one output slot on one rank:
+//   DONE  -- rows-written counter, bumped once per finished (sequence, kv head)
+//            by the writing CTA of every rank (system-scope release add);
+//   USES  -- completed uses of the slot on this rank (local);
+//   ERR   -- set when a spin times out;
+//   ARR   -- grid arrival counter of the running K2 (self-resetting);
+//   FREE+i -- uses of the slot rank i has released (written by rank i).
+// ---------------------------------------------------------------------------
+constexpr int CTL_DONE = 0, CTL_USES = 1, CTL_ERR = 2, CTL_ARR = 3, CTL_FREE = 32;
+constexpr unsigned long long SPIN_TIMEOUT_NS = 10ull * 1000 * 1000 * 1000;
+
+__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* a) {
+  uint32_t v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_sys(uint32_t* a, uint32_t v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(a), "r"(v) : "memory");
+}
+__device__ __forceinline__ void red_add_release_sys(uint32_t* a, uint32_t v) {
+  asm volatile("red.release.sys.global.add.u32 [%0], %1;" ::"l"(a), "r"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long global_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+// Spin until (int)(*w - target) >= 0; on timeout set the error word and give up.
+__device__ __noinline__ void spin_until(const uint32_t* w, uint32_t target, uint32_t* err) {
+  const unsigned long long t0 = global_ns();
+  while ((int)(ld_acquire_sys(w) - target) < 0) {
+    if (global_ns() - t0 > SPIN_TIMEOUT_NS) {
+      atomicExch(err, 1u);
+      return;
+    }
+    __nanosleep(64);
+  }
+}
+__device__ __forceinline__ uint32_t* peer_ctl(const kvq_peer_out& pe, int r) {
+  return reinterpret_cast<uint32_t*>(pe.ctl[r]);
+}
+// CTA entry (thread 0): this rank has consumed every earlier use of the slot
+// (stream order), so release them to every writer.  Idempotent per CTA.
+__device__ __forceinline__ void peer_release(const kvq_peer_out& pe) {
+  const uint32_t uses = *reinterpret_cast<volatile uint32_t*>(peer_ctl(pe, pe.rank) + CTL_USES);
+  for (int r = 0; r < pe.n_peers; ++r) st_release_sys(peer_ctl(pe, r) + CTL_FREE + pe.rank, uses);
+}
+// Before a CTA's final output stores: every rank must have released the slot's previous use.
+__device__ __forceinline__ void peer_acquire(const kvq_peer_out& pe) {
+  if (threadIdx.x == 0) {
+    uint32_t* mine = peer_ctl(pe, pe.rank);
+    const uint32_t uses = *reinterpret_cast<volatile uint32_t*>(mine + CTL_USES);
+    for (int r = 0; r < pe.n_peers; ++r) spin_until(mine + CTL_FREE + r, uses, mine + CTL_ERR);
+  }
+  __syncthreads();
+}
+// After a CTA's final output stores: publish them (system scope) and count one writer on every rank.
+__device__ __forceinline__ void peer_signal(const kvq_peer_out& pe) {
+  __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x == 0)
+    for (int r = 0; r < pe.n_peers; ++r) red_add_release_sys(peer_ctl(pe, r) + CTL_DONE, 1u);
+}
+// CTA exit (thread 0): the last CTA of the grid waits until every rank's rows of
+// this use have landed here, then counts the use.  K2 completing == gather done.
+__device__ __forceinline__ void peer_arrive(const kvq_peer_out& pe) {
+  uint32_t* mine = peer_ctl(pe, pe.rank);
+  const uint32_t total = gridDim.x * gridDim.y * gridDim.z;
+  uint32_t prev;
+  asm volatile("atom.add.acq_rel.gpu.u32 %0, [%1], 1;" : "=r"(prev) : "l"(mine + CTL_ARR) : "memory");
+  if (prev != total - 1) return;
+  mine[CTL_ARR] = 0;
+  const uint32_t uses = *reinterpret_cast<volatile uint32_t*>(mine + CTL_USES);
+  spin_until(mine + CTL_DONE, (uses + 1) * pe.writers_per_use, mine + CTL_ERR);
+  *reinterpret_cast<volatile uint32_t*>(mine + CTL_USES) = uses + 1;
+  __threadfence();
+}
+
 // Query row j of kv head h (j < G) is query token i = j / g of head h*g + j % g.
 // Output rows are query tokens t = b * q_len + i: [T][Hq][d] or head-major [Hq][T][d].
+template <bool PEER>
 __device__ __forceinline__ void store_out(const DecodeParams& p, int b, int h, int j, int d0,
                                           const float* vals) {
   const int i = j / p.g, head = h * p.g + j % p.g;
+  if constexpr (PEER) {  // fused gather: bf16 row into every rank's global [Hq][B][d]
+    const int gb = p.peer.seq_map ? __ldg(p.peer.seq_map + b) : b;
+    const int64_t grow = (int64_t)(p.peer.head_offset + head) * p.peer.batch_global + gb;
+    uint4 w;
+    w.x = pack_bf16x2(vals[0], vals[1]);
+    w.y = pack_bf16x2(vals[2], vals[3]);
+    w.z = pack_bf16x2(vals[4], vals[5]);
+    w.w = pack_bf16x2(vals[6], vals[7]);
+    for (int r = 0; r < p.peer.n_peers; ++r)
+      *reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(p.peer.out[r]) + grow * HD + d0) = w;
+    return;
+  }
   const int64_t t = (int64_t)b * p.q_len + i;
   const int64_t row = p.out_hbd ? ((int64_t)head * p.B * p.q_len + t) : (t * p.Hq + head);
   if (p.out_f32) {
@@ -514,11 +614,12 @@ struct PageStream {
 // movmatrix transpose per 8x8 block.  d is permuted inside each k-step /
 // m-tile so every thread reads 16-byte chunks (bank-conflict-free given the
 // page swizzle).
-template <int KVD, bool HI, bool MQ>
-__global__ void __launch_bounds__(THREADS, Geo<HI>::CTAS) decode_kernel(const DecodeParams p) {
+// MODE: 0 = decode, 1 = multi-query (q_len > 1), 2 = decode with the fused peer gather.
+template <int KVD, bool HI, int MODE>
+__device__ __forceinline__ void decode_cta(const DecodeParams& p, uint8_t* smem) {
+  constexpr bool MQ = MODE == 1, PEER = MODE == 2;
   constexpr int NT = Geo<HI>::NT;
   constexpr int S = Geo<HI>::S;
-  extern __shared__ __align__(128) uint8_t smem[];
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + NW * S * PAGE);
   int* flag = reinterpret_cast<int*>(bars + NW * S);
   uint2* qsm = reinterpret_cast<uint2*>(smem + NW * S * PAGE + NW * S * sizeof(uint64_t) + 16);
@@ -533,9 +634,11 @@ __global__ void __launch_bounds__(THREADS, Geo<HI>::CTAS) decode_kernel(const De
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   if (L <= 0) {  // empty sequence: zeros, nothing to combine
+    if constexpr (PEER) peer_acquire(p.peer);
     const float z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     for (int idx = threadIdx.x; idx < G * (HD / 8); idx += THREADS)
-      store_out(p, b, h, idx / (HD / 8), (idx % (HD / 8)) * 8, z);
+      store_out<PEER>(p, b, h, idx / (HD / 8), (idx % (HD / 8)) * 8, z);
+    if constexpr (PEER) peer_signal(p.peer);
     return;
   }
   const int pg0 = split * p.pages_per_split;
@@ -972,6 +1075,7 @@ __global__ void __launch_bounds__(THREADS, Geo<HI>::CTAS) decode_kernel(const De
     }
   }
   __syncthreads();
+  if (PEER && nsplit == 1) peer_acquire(p.peer);
   // Each thread finalises 8 contiguous d of one head row.
   const int tid = threadIdx.x;
   const int nrow_items = G * (HD / 8);
@@ -996,7 +1100,7 @@ __global__ void __launch_bounds__(THREADS, Geo<HI>::CTAS) decode_kernel(const De
     for (int e = 0; e < 8; ++e) acc[e] *= inv;
     const int64_t vrow = ((int64_t)b * p.Hkv + h) * G + row;  // partial row of (b, h, query row)
     if (nsplit == 1) {
-      store_out(p, b, h, row, d0, acc);
+      store_out<PEER>(p, b, h, row, d0, acc);
     } else {
       float* dst = p.part_o + (vrow * p.max_splits + split) * HD + d0;
       *reinterpret_cast<float4*>(dst) = make_float4(acc[0], acc[1], acc[2], acc[3]);
@@ -1004,7 +1108,10 @@ __global__ void __launch_bounds__(THREADS, Geo<HI>::CTAS) decode_kernel(const De
       if (d0 == 0) p.part_lse[vrow * p.max_splits + split] = M + __log2f(lsum);
     }
   }
-  if (nsplit == 1) return;
+  if (nsplit == 1) {
+    if constexpr (PEER) peer_signal(p.peer);
+    return;
+  }
 
   // ===== fused split-KV combine: the last CTA of (b, h) merges all splits =====
   // Every thread fences its partial stores at gpu scope before the barrier;
@@ -1022,6 +1129,7 @@ __global__ void __launch_bounds__(THREADS, Geo<HI>::CTAS) decode_kernel(const De
   }
   __syncthreads();
   if (!*flag) return;
+  if constexpr (PEER) peer_acquire(p.peer);
   for (int item = tid; item < nrow_items; item += THREADS) {
     const int row = item / (HD / 8), d0 = (item % (HD / 8)) * 8;
     const int64_t base = (((int64_t)b * p.Hkv + h) * G + row) * p.max_splits;
@@ -1047,8 +1155,17 @@ __global__ void __launch_bounds__(THREADS, Geo<HI>::CTAS) decode_kernel(const De
     const float inv = 1.0f / wsum;
 #pragma unroll
     for (int e = 0; e < 8; ++e) acc[e] *= inv;
-    store_out(p, b, h, row, d0, acc);
+    store_out<PEER>(p, b, h, row, d0, acc);
   }
+  if constexpr (PEER) peer_signal(p.peer);
+}
+
+template <int KVD, bool HI, int MODE>
+__global__ void __launch_bounds__(THREADS, Geo<HI>::CTAS) decode_kernel(const DecodeParams p) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  if (MODE == 2 && threadIdx.x == 0) peer_release(p.peer);
+  decode_cta<KVD, HI, MODE>(p, smem);
+  if (MODE == 2 && threadIdx.x == 0) peer_arrive(p.peer);
 }
 
 // ---------------------------------------------------------------------------
@@ -1189,12 +1306,12 @@ int32_t kvq_decode_pages_per_split(int32_t B, int32_t Hkv, int64_t total_pages, 
   return (int32_t)(pps > 0 ? pps : 1);
 }
 
-int kvq_decode_attn_mq(const void* q, int64_t q_batch_stride, int32_t q_len, const void* pool,
-                       int64_t num_blocks, const int32_t* block_table, int32_t max_blocks,
-                       const int32_t* seq_lens, int32_t B, int32_t Hq, int32_t Hkv, int32_t kv_dtype,
-                       float sm_scale, int32_t pages_per_split, void* workspace,
-                       size_t workspace_bytes, void* out, int32_t out_dtype, int32_t out_layout,
-                       void* stream) {
+static int decode_attn_impl(const void* q, int64_t q_batch_stride, int32_t q_len, const void* pool,
+                            int64_t num_blocks, const int32_t* block_table, int32_t max_blocks,
+                            const int32_t* seq_lens, int32_t B, int32_t Hq, int32_t Hkv, int32_t kv_dtype,
+                            float sm_scale, int32_t pages_per_split, void* workspace,
+                            size_t workspace_bytes, void* out, int32_t out_dtype, int32_t out_layout,
+                            const kvq_peer_out* peer, void* stream) {
   if (B < 0 || Hq <= 0 || Hkv <= 0 || max_blocks <= 0 || num_blocks <= 0 || q_len <= 0)
     return fail(KVQ_EINVAL, "decode_attn: bad sizes");
   if (B == 0) return KVQ_OK;
@@ -1245,6 +1362,8 @@ int kvq_decode_attn_mq(const void* q, int64_t q_batch_stride, int32_t q_len, con
   prm.out = out;
   prm.out_f32 = out_dtype == KVQ_OUT_F32;
   prm.out_hbd = out_layout == KVQ_OUT_HBD;
+  prm.peer = kvq_peer_out{};
+  if (peer) prm.peer = *peer;
 
   const dim3 grid((unsigned)max_splits, (unsigned)Hkv, (unsigned)B);
   auto st = static_cast<cudaStream_t>(stream);
@@ -1260,16 +1379,84 @@ int kvq_decode_attn_mq(const void* q, int64_t q_batch_stride, int32_t q_len, con
     kernel<<<grid, kvq::THREADS, smem_bytes, st>>>(prm);
     return check_launch("decode_attn");
   };
-  const bool mq = q_len > 1;
+  const int mode = peer ? 2 : (q_len > 1 ? 1 : 0);
   if (kv_dtype == KVQ_INT8) {
-    if (mq) return hi ? launch(kvq::decode_kernel<KVQ_INT8, true, true>) : launch(kvq::decode_kernel<KVQ_INT8, false, true>);
-    return hi ? launch(kvq::decode_kernel<KVQ_INT8, true, false>) : launch(kvq::decode_kernel<KVQ_INT8, false, false>);
+    if (mode == 2) return hi ? launch(kvq::decode_kernel<KVQ_INT8, true, 2>) : launch(kvq::decode_kernel<KVQ_INT8, false, 2>);
+    if (mode == 1) return hi ? launch(kvq::decode_kernel<KVQ_INT8, true, 1>) : launch(kvq::decode_kernel<KVQ_INT8, false, 1>);
+    return hi ? launch(kvq::decode_kernel<KVQ_INT8, true, 0>) : launch(kvq::decode_kernel<KVQ_INT8, false, 0>);
   }
-  if (mq)
-    return hi ? launch(kvq::decode_kernel<KVQ_FP8_E4M3, true, true>)
-              : launch(kvq::decode_kernel<KVQ_FP8_E4M3, false, true>);
-  return hi ? launch(kvq::decode_kernel<KVQ_FP8_E4M3, true, false>)
-            : launch(kvq::decode_kernel<KVQ_FP8_E4M3, false, false>);
+  if (mode == 2)
+    return hi ? launch(kvq::decode_kernel<KVQ_FP8_E4M3, true, 2>) : launch(kvq::decode_kernel<KVQ_FP8_E4M3, false, 2>);
+  if (mode == 1)
+    return hi ? launch(kvq::decode_kernel<KVQ_FP8_E4M3, true, 1>) : launch(kvq::decode_kernel<KVQ_FP8_E4M3, false, 1>);
+  return hi ? launch(kvq::decode_kernel<KVQ_FP8_E4M3, true, 0>) : launch(kvq::decode_kernel<KVQ_FP8_E4M3, false, 0>);
+}
+
+int kvq_decode_attn_mq(const void* q, int64_t q_batch_stride, int32_t q_len, const void* pool,
+                       int64_t num_blocks, const int32_t* block_table, int32_t max_blocks,
+                       const int32_t* seq_lens, int32_t B, int32_t Hq, int32_t Hkv, int32_t kv_dtype,
+                       float sm_scale, int32_t pages_per_split, void* workspace,
+                       size_t workspace_bytes, void* out, int32_t out_dtype, int32_t out_layout,
+                       void* stream) {
+  return decode_attn_impl(q, q_batch_stride, q_len, pool, num_blocks, block_table, max_blocks, seq_lens, B,
+                          Hq, Hkv, kv_dtype, sm_scale, pages_per_split, workspace, workspace_bytes, out,
+                          out_dtype, out_layout, nullptr, stream);
+}
+
+int kvq_decode_attn_peer(const void* q, int64_t q_batch_stride, const void* pool, int64_t num_blocks,
+                         const int32_t* block_table, int32_t max_blocks, const int32_t* seq_lens,
+                         int32_t B, int32_t Hq, int32_t Hkv, int32_t kv_dtype, float sm_scale,
+                         int32_t pages_per_split, void* workspace, size_t workspace_bytes,
+                         const kvq_peer_out* peer, void* stream) {
+  if (!peer) return fail(KVQ_EINVAL, "decode_attn_peer: null peer descriptor");
+  const int P = peer->n_peers;
+  if (P < 2 || P > KVQ_MAX_PEERS || peer->rank < 0 || peer->rank >= P)
+    return fail(KVQ_EINVAL, "decode_attn_peer: need 2 <= n_peers <= 8 and 0 <= rank < n_peers");
+  if (peer->head_offset < 0 || peer->batch_global < B || peer->writers_per_use == 0)
+    return fail(KVQ_EINVAL, "decode_attn_peer: bad head_offset / batch_global / writers_per_use");
+  for (int r = 0; r < P; ++r)
+    if (!peer->out[r] || !peer->ctl[r] || !aligned(peer->out[r], 16) || !aligned(peer->ctl[r], 128))
+      return fail(KVQ_EINVAL, "decode_attn_peer: peer out (16 B) / ctl (128 B) pointers missing or misaligned");
+  // `out` is not written in peer mode; the rank's own copy stands in for validation.
+  return decode_attn_impl(q, q_batch_stride, 1, pool, num_blocks, block_table, max_blocks, seq_lens, B, Hq,
+                          Hkv, kv_dtype, sm_scale, pages_per_split, workspace, workspace_bytes,
+                          peer->out[peer->rank], KVQ_OUT_BF16, KVQ_OUT_HBD, peer, stream);
+}
+
+int kvq_sym_alloc(size_t bytes, void** ptr, void* ipc_handle) {
+  if (!ptr || !ipc_handle || bytes == 0) return fail(KVQ_EINVAL, "sym_alloc: bad arguments");
+  void* p = nullptr;
+  cudaError_t e = cudaMalloc(&p, bytes);
+  if (e == cudaSuccess) e = cudaMemset(p, 0, bytes);
+  cudaIpcMemHandle_t h;
+  if (e == cudaSuccess) e = cudaIpcGetMemHandle(&h, p);
+  if (e != cudaSuccess) {
+    if (p) cudaFree(p);
+    return fail(KVQ_ECUDA, cudaGetErrorString(e));
+  }
+  static_assert(sizeof(h) == KVQ_IPC_HANDLE_BYTES, "IPC handle size");
+  memcpy(ipc_handle, &h, sizeof(h));
+  *ptr = p;
+  return KVQ_OK;
+}
+
+int kvq_sym_open(const void* ipc_handle, void** ptr) {
+  if (!ptr || !ipc_handle) return fail(KVQ_EINVAL, "sym_open: bad arguments");
+  cudaIpcMemHandle_t h;
+  memcpy(&h, ipc_handle, sizeof(h));
+  const cudaError_t e = cudaIpcOpenMemHandle(ptr, h, cudaIpcMemLazyEnablePeerAccess);
+  if (e != cudaSuccess) return fail(KVQ_ECUDA, cudaGetErrorString(e));
+  return KVQ_OK;
+}
+
+int kvq_sym_close(void* ptr) {
+  const cudaError_t e = cudaIpcCloseMemHandle(ptr);
+  return e == cudaSuccess ? KVQ_OK : fail(KVQ_ECUDA, cudaGetErrorString(e));
+}
+
+int kvq_sym_free(void* ptr) {
+  const cudaError_t e = cudaFree(ptr);
+  return e == cudaSuccess ? KVQ_OK : fail(KVQ_ECUDA, cudaGetErrorString(e));
 }
 
 int kvq_decode_attn(const void* q, int64_t q_batch_stride, const void* pool, int64_t num_blocks,

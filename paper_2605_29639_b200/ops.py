@@ -4,6 +4,8 @@ on a CUDA device, or a missing library, raises.
 
 * :func:`quantize_append`       -> ``kvq_quant_append``  (K1)
 * :func:`paged_decode_attention` -> ``kvq_decode_attn``  (K2 + fused combine)
+* :func:`paged_decode_attention_gathered` -> ``kvq_decode_attn_peer`` (K2 with
+  the KV-head output all-gather fused in, over peer memory)
 * :func:`copy_blocks`            -> ``kvq_copy_blocks``  (copy-on-write pages)
 """
 from __future__ import annotations
@@ -147,6 +149,57 @@ def paged_decode_attention(q: torch.Tensor, cache: PagedKVCache, block_table: to
         _lib.KVQ_OUT_HBD if head_major else _lib.KVQ_OUT_BHD, _stream_handle(q.device))
     _lib.check("kvq_decode_attn", st)
     return out
+
+
+def paged_decode_attention_gathered(q: torch.Tensor, cache: PagedKVCache, block_table: torch.Tensor,
+                                    seq_lens: torch.Tensor, peer, slot: int = 0, *,
+                                    sm_scale: Optional[float] = None,
+                                    pages_per_split: Optional[int] = None,
+                                    total_pages: Optional[int] = None,
+                                    workspace: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """KV-head-sharded decode attention with the output all-gather fused into
+    K2 (``kvq_decode_attn_peer``): this rank attends its sequences over its
+    heads (``q``: bf16 ``[B_r, Hq_r, 128]``) and every finished row is stored
+    into all ranks' copies of the global output.  ``peer`` is a
+    :class:`paper_2605_29639_b200.shard.PeerOutput`; returns its ``out(slot)``
+    (``[Hq, B, 128]`` bf16), complete on this rank once the launch completes."""
+    _require_cuda("paged_decode_attention_gathered", q, block_table, seq_lens, cache.pool)
+    spec = cache.spec
+    if q.dtype != torch.bfloat16 or q.dim() != 3 or q.shape[-1] != 128 or q.stride(-1) != 1 \
+            or q.stride(-2) != 128:
+        raise ValueError("paged_decode_attention_gathered: q must be bf16 [B, Hq, 128] with contiguous heads")
+    B, Hq = q.shape[0], q.shape[1]
+    if block_table.dtype != torch.int32 or block_table.dim() != 2 or block_table.shape[0] != B \
+            or not block_table.is_contiguous():
+        raise ValueError("paged_decode_attention_gathered: block_table must be contiguous int32 [B, max_blocks]")
+    if seq_lens.dtype != torch.int32 or seq_lens.shape != (B,) or not seq_lens.is_contiguous():
+        raise ValueError("paged_decode_attention_gathered: seq_lens must be contiguous int32 [B]")
+    if not 0 <= slot < peer.slots:
+        raise ValueError("paged_decode_attention_gathered: bad slot")
+    if peer.plan.q_range[1] - peer.plan.q_range[0] != Hq:
+        raise ValueError("paged_decode_attention_gathered: q heads do not match the shard plan")
+    if B == 0:
+        return peer.out(slot)
+    if sm_scale is None:
+        sm_scale = 1.0 / math.sqrt(128)
+    lib = _lib.load()
+    max_blocks = block_table.shape[1]
+    pps = pages_per_split or lib.kvq_decode_pages_per_split(
+        B, spec.num_kv_heads, total_pages if total_pages is not None else B * max_blocks, max_blocks)
+    max_splits = -(-max_blocks // pps)
+    nbytes = lib.kvq_decode_workspace_bytes(B, Hq, spec.num_kv_heads, max_splits)
+    if workspace is None:
+        workspace = _workspace(q.device, nbytes, ((B * spec.num_kv_heads * 4 + 255) // 256) * 256)
+    elif workspace.numel() * workspace.element_size() < nbytes:
+        raise ValueError(f"paged_decode_attention_gathered: workspace needs {nbytes} bytes")
+    import ctypes
+    st = lib.kvq_decode_attn_peer(
+        q.data_ptr(), q.stride(0), cache.pool.data_ptr(), cache.num_blocks, block_table.data_ptr(),
+        max_blocks, seq_lens.data_ptr(), B, Hq, spec.num_kv_heads, spec.kv_dtype_id, float(sm_scale),
+        int(pps), workspace.data_ptr(), workspace.numel() * workspace.element_size(),
+        ctypes.addressof(peer.descs[slot]), _stream_handle(q.device))
+    _lib.check("kvq_decode_attn_peer", st)
+    return peer.out(slot)
 
 
 def copy_blocks(cache: PagedKVCache, pairs: Sequence[Tuple[int, int]]) -> None:

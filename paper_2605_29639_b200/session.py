@@ -26,26 +26,35 @@ import torch
 
 from . import _lib
 from .cache import PagedKVCache
-from .ops import paged_decode_attention, quantize_append, workspace_bytes
+from .ops import paged_decode_attention, paged_decode_attention_gathered, quantize_append, workspace_bytes
 
 
 class DecodeSession:
     def __init__(self, cache: PagedKVCache, block_table: torch.Tensor, batch: int, num_q_heads: int,
                  *, total_pages: Optional[int] = None, out_dtype: torch.dtype = torch.bfloat16,
                  head_major: bool = False, sm_scale: Optional[float] = None, depth: int = 2,
-                 gather_factory=None, pages_per_split: Optional[int] = None, graphs: bool = False):
+                 gather_factory=None, pages_per_split: Optional[int] = None, graphs: bool = False,
+                 peer=None):
         """With ``gather_factory`` (returning a
         :class:`paper_2605_29639_b200.shard.OutputGather`, one per buffer slot,
         for KV-head / 2-D sharding) the local head-major output
         ``[Hq_loc, B_r, d]`` is assembled into ``[Hq, B, d]`` on the compute
         stream before the download.
 
+        With ``peer`` (a :class:`paper_2605_29639_b200.shard.PeerOutput`
+        with ``slots >= depth``) the gather is fused into K2 instead: each
+        buffer slot's K2 stores its rows into every rank's copy of the global
+        output over peer memory, and the download reads the slot's copy.
+
         With ``graphs=True`` each buffer slot's device work (K1, K2 and the
         gather) is captured once as a CUDA graph on first use and replayed by
         every later :meth:`submit`: one host call per step instead of one
         per kernel."""
         dev = cache.device
-        self.sharded = gather_factory is not None
+        self.peer = peer
+        if peer is not None and (gather_factory is not None or peer.slots < depth):
+            raise ValueError("DecodeSession: peer needs slots >= depth and no gather_factory")
+        self.sharded = gather_factory is not None or peer is not None
         if self.sharded:
             head_major = True
         self.cache, self.block_table = cache, block_table
@@ -82,7 +91,7 @@ class DecodeSession:
             return {name: blob[o: o + nb].view(dt).view(shape) for name, shape, dt, o, nb in layout}
 
         self.bufs = []
-        for _ in range(depth):
+        for i in range(depth):
             dev_in = torch.empty(max(off, 16), dtype=torch.uint8, device=dev)
             host_in = torch.empty(max(off, 16), dtype=torch.uint8, pin_memory=pin)
             self.bufs.append(dict(
@@ -91,7 +100,7 @@ class DecodeSession:
                 ws=torch.zeros(workspace_bytes(batch, num_q_heads, self.Hkv, max_splits),
                                dtype=torch.uint8, device=dev),
                 in_ready=torch.cuda.Event(), done=torch.cuda.Event(), out_done=torch.cuda.Event(),
-                gather=gather_factory() if self.sharded else None, used=False))
+                gather=gather_factory() if gather_factory is not None else None, used=False, idx=i))
         self.step_idx = 0
         self.graphs = graphs
 
@@ -100,7 +109,13 @@ class DecodeSession:
         quantize_append(self.cache, buf["k"], buf["v"], buf["slots"])
 
     def k2(self, buf) -> None:
-        """Paged decode attention over the cache into ``buf["out"]``."""
+        """Paged decode attention over the cache into ``buf["out"]`` (or, with
+        ``peer``, into every rank's copy of the slot's global output)."""
+        if self.peer is not None:
+            paged_decode_attention_gathered(buf["q"], self.cache, self.block_table, buf["lens"], self.peer,
+                                            buf["idx"], sm_scale=self.sm_scale, pages_per_split=self.pps,
+                                            workspace=buf["ws"])
+            return
         paged_decode_attention(buf["q"], self.cache, self.block_table, buf["lens"], out=buf["out"],
                                head_major=self.head_major, sm_scale=self.sm_scale,
                                pages_per_split=self.pps, out_dtype=self.out_dtype,
@@ -156,20 +171,25 @@ class DecodeSession:
         one host-to-device copy, the device step, one device-to-host copy."""
         return self._submit(None, out_h)
 
+    def _result(self, buf) -> torch.Tensor:
+        if self.peer is not None:
+            return self.peer.out(buf["idx"])
+        return buf["gather"](buf["out"]) if buf["gather"] is not None else buf["out"]
+
     def _device_step(self, buf) -> torch.Tensor:
         if not self.graphs:
             self._kernels(buf)
-            return buf["gather"](buf["out"]) if self.sharded else buf["out"]
+            return self._result(buf)
         g = buf.get("graph")
         if g is None:
             # Warm once eagerly (module load, NCCL communicator), then capture.
             self._kernels(buf)
-            full = buf["gather"](buf["out"]) if self.sharded else buf["out"]
+            full = self._result(buf)
             self.compute.synchronize()
             g = torch.cuda.CUDAGraph()
             with torch.cuda.graph(g, stream=torch.cuda.Stream(self.cache.device)):
                 self._kernels(buf)
-                full = buf["gather"](buf["out"]) if self.sharded else buf["out"]
+                full = self._result(buf)
             buf["graph"], buf["graph_out"] = g, full
         buf["graph"].replay()
         return buf["graph_out"]

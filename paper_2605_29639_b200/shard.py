@@ -216,3 +216,109 @@ def cuda_local_attention(cache, block_table, seq_lens, **kw) -> Callable[[torch.
         return paged_decode_attention(q_loc, cache, block_table, seq_lens, head_major=True, **kw)
 
     return run
+
+
+class _RawCuda:
+    """``__cuda_array_interface__`` wrapper so torch can view memory that libkvq
+    allocated (the symmetric buffers are not torch allocations)."""
+
+    def __init__(self, ptr: int, shape, typestr: str):
+        self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": typestr,
+                                         "data": (int(ptr), False), "version": 3, "strides": None}
+
+
+class PeerOutput:
+    """Symmetric output buffers for the all-gather fused into K2.
+
+    Every rank allocates ``slots`` x (control block + global bf16 output
+    ``[Hq, B, 128]``) with ``kvq_sym_alloc``, the IPC handles are exchanged
+    once over ``group`` (any backend; this is setup, not the step path) and
+    each rank maps all peers' buffers.  :func:`ops.paged_decode_attention_gathered`
+    then runs K2 with ``kvq_peer_out`` so each finished row is stored into
+    every rank's copy over NVLink while the attention streams; when the launch
+    completes on a rank, :meth:`out` holds all ranks' heads -- there is no
+    separate collective.  With the 2-D partition (``plan.b_split > 1``) each
+    rank's rows land at their global batch positions through ``seq_map``.
+
+    Slot reuse is protected on the device (K2 releases a slot's previous use
+    at entry and writers wait for every rank's release), so callers only keep
+    the usual stream order: consume slot s's output before the next K2 that
+    uses slot s is enqueued on the same stream (DecodeSession does, through
+    its per-slot events)."""
+
+    def __init__(self, plan: ShardPlan, num_q_heads: int, batch: int, num_kv_heads: int,
+                 device: torch.device, group: Optional[dist.ProcessGroup] = None, slots: int = 1):
+        import ctypes
+
+        from . import _lib
+        lib = _lib.load()
+        if not 2 <= plan.world <= _lib.MAX_PEERS:
+            raise ValueError(f"fused gather needs 2..{_lib.MAX_PEERS} ranks, got {plan.world}")
+        self.plan, self.P, self.rank, self.slots = plan, plan.world, plan.rank, slots
+        self.Hq, self.B, self.device = num_q_heads, batch, torch.device(device)
+        self.out_bytes = num_q_heads * batch * 128 * 2
+        self.slot_bytes = _lib.PEER_CTL_BYTES + ((self.out_bytes + 255) // 256) * 256
+        with torch.cuda.device(self.device):
+            ptr, handle = ctypes.c_void_p(), (ctypes.c_char * _lib.IPC_HANDLE_BYTES)()
+            _lib.check("kvq_sym_alloc", lib.kvq_sym_alloc(slots * self.slot_bytes, ctypes.byref(ptr), handle))
+            self._own = ptr.value
+            handles: List[Optional[bytes]] = [None] * self.P
+            dist.all_gather_object(handles, bytes(handle), group=group)
+            self._bases, self._opened = [], []
+            for r, h in enumerate(handles):
+                if r == self.rank:
+                    self._bases.append(self._own)
+                    continue
+                p = ctypes.c_void_p()
+                _lib.check("kvq_sym_open", lib.kvq_sym_open(h, ctypes.byref(p)))
+                self._bases.append(p.value)
+                self._opened.append(p.value)
+        self.group = group
+        # rows of this rank's sequences in the global output (identity for a pure head split)
+        self.seq_map = (None if plan.b_split == 1 else
+                        torch.as_tensor(plan.seqs.astype(np.int32), device=self.device))
+        self.writers_per_use = batch * num_kv_heads  # every global (sequence, kv head) writes once
+        self.descs = []
+        for s in range(slots):
+            d = _lib.PeerOutDesc()
+            d.n_peers, d.rank = self.P, self.rank
+            d.head_offset, d.batch_global = plan.q_range[0], batch
+            d.seq_map = self.seq_map.data_ptr() if self.seq_map is not None else None
+            d.writers_per_use = self.writers_per_use
+            for r in range(self.P):
+                d.ctl[r] = self._bases[r] + s * self.slot_bytes
+                d.out[r] = self._bases[r] + s * self.slot_bytes + _lib.PEER_CTL_BYTES
+            self.descs.append(d)
+        self._outs = [torch.as_tensor(_RawCuda(self._own + s * self.slot_bytes + _lib.PEER_CTL_BYTES,
+                                               (num_q_heads, batch, 128), "<i2"), device=self.device)
+                      .view(torch.bfloat16) for s in range(slots)]
+        self._ctls = [torch.as_tensor(_RawCuda(self._own + s * self.slot_bytes, (_lib.PEER_CTL_BYTES // 4,),
+                                               "<i4"), device=self.device) for s in range(slots)]
+        dist.barrier(group=group)  # every rank mapped before anyone writes
+
+    def out(self, slot: int = 0) -> torch.Tensor:
+        """This rank's copy of the global output ``[Hq, B, 128]`` (bf16) of ``slot``."""
+        return self._outs[slot]
+
+    def control(self, slot: int = 0) -> torch.Tensor:
+        """int32 view of the slot's control block (done, uses, error, arrivals, free[P])."""
+        return self._ctls[slot]
+
+    def errors(self) -> int:
+        """Number of slots whose protocol spin timed out (synchronises)."""
+        return int(sum(int(c[2].item() != 0) for c in self._ctls))
+
+    def close(self) -> None:
+        """Unmap peers and free this rank's buffer (collective: barrier first,
+        so no peer still writes into it)."""
+        from . import _lib
+        if self._own is None:
+            return
+        torch.cuda.synchronize(self.device)
+        dist.barrier(group=self.group)
+        lib = _lib.load()
+        with torch.cuda.device(self.device):
+            for p in self._opened:
+                lib.kvq_sym_close(p)
+            lib.kvq_sym_free(self._own)
+        self._own, self._opened, self._outs, self._ctls = None, [], [], []

@@ -18,7 +18,7 @@ def declared_functions():
 
 def test_header_matches_binding():
     names = declared_functions()
-    assert len(names) == 10
+    assert len(names) == 15
     assert set(names) == set(_lib.SIGNATURES)
 
 
@@ -51,6 +51,29 @@ def test_argument_validation_without_gpu():
     assert L.kvq_copy_blocks(None, 1, 1, None, 0, None) == 0   # no-op
     with pytest.raises(ValueError):
         _lib.check("kvq_decode_attn", _lib.KVQ_EINVAL)
+
+
+def test_peer_descriptor_validation_without_gpu():
+    """kvq_decode_attn_peer rejects a bad kvq_peer_out before touching the device;
+    the ctypes struct mirrors the C layout."""
+    L = _lib.load()
+    assert ctypes.sizeof(_lib.PeerOutDesc) == 4 * 4 + 8 + 4 + 4 + 2 * 8 * _lib.MAX_PEERS
+    args = (16, 4096, 16, 10, 16, 4, 16, 2, 32, 8, 0, 0.1, 0, 256, 1 << 20)
+    assert L.kvq_decode_attn_peer(*args, None, None) == _lib.KVQ_EINVAL
+    d = _lib.PeerOutDesc()
+    d.n_peers, d.rank, d.batch_global, d.writers_per_use = 1, 0, 2, 16
+    assert L.kvq_decode_attn_peer(*args, ctypes.addressof(d), None) == _lib.KVQ_EINVAL
+    assert b"n_peers" in L.kvq_last_error()
+    d.n_peers = 2
+    assert L.kvq_decode_attn_peer(*args, ctypes.addressof(d), None) == _lib.KVQ_EINVAL
+    assert b"misaligned" in L.kvq_last_error()        # null peer buffers
+    d.out[0], d.out[1], d.ctl[0], d.ctl[1] = 256, 512, 1024, 1040   # ctl[1] not 128-byte aligned
+    assert L.kvq_decode_attn_peer(*args, ctypes.addressof(d), None) == _lib.KVQ_EINVAL
+    d.ctl[1] = 1152
+    d.batch_global = 1                                  # < B
+    assert L.kvq_decode_attn_peer(*args, ctypes.addressof(d), None) == _lib.KVQ_EINVAL
+    h = (ctypes.c_char * _lib.IPC_HANDLE_BYTES)()
+    assert L.kvq_sym_alloc(0, ctypes.byref(ctypes.c_void_p()), h) == _lib.KVQ_EINVAL
 
 
 def test_ops_refuse_cpu_tensors():

@@ -21,6 +21,8 @@
 #include <stdio.h>
 #include <string.h>
 
+#include <type_traits>
+
 #include "kvq.h"
 
 namespace kvq {
@@ -320,6 +322,20 @@ __device__ __forceinline__ uint4 lds128(const uint8_t* p) {
   asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
                : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
                : "r"(smem_u32(p)));
+  return r;
+}
+template <int OFF>
+__device__ __forceinline__ uint4 lds128_at(uint32_t a) {
+  uint4 r;
+  asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4+%5];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "r"(a), "n"(OFF));
+  return r;
+}
+template <int OFF>
+__device__ __forceinline__ float lds32f_at(uint32_t a) {
+  float r;
+  asm volatile("ld.shared.f32 %0, [%1+%2];" : "=f"(r) : "r"(a), "n"(OFF));
   return r;
 }
 __device__ __forceinline__ float lds32f(const uint8_t* p) {
@@ -713,7 +729,7 @@ __device__ __forceinline__ void decode_cta(const DecodeParams& p, uint8_t* smem)
       // qf[nt][2j] = term 1 (b0, b1), qf[nt][2j + 1] = term 2.
       const float s1 = amax / 127.0f;
       const float inv1 = amax > 0.0f ? 127.0f / amax : 0.0f;
-      qscale = p.sm_scale_log2 * s1;
+      qscale = p.sm_scale_log2 * s1 * 0.0078125f;  // S = s1 * (128 acc1 + acc2) / 128
 #pragma unroll
       for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
@@ -771,17 +787,19 @@ __device__ __forceinline__ void decode_cta(const DecodeParams& p, uint8_t* smem)
     __syncthreads();
   }
 
-  // Per-thread smem offsets inside a page (fixed for every page).
-  // K unit j of row pair r = {K[r][16c+4j..], K[r+8][16c+4j..], K[r][64+16c+4j..], K[r+8][64+16c+4j..]}
-  const int koff0 = r * 256 + (((0 + c) ^ ((r & 1) << 2)) << 4);
-  const int koff1 = r * 256 + (((4 + c) ^ ((r & 1) << 2)) << 4);
-  const int koff2 = r * 256 + (((8 + c) ^ ((r & 1) << 2)) << 4);
-  const int koff3 = r * 256 + (((12 + c) ^ ((r & 1) << 2)) << 4);
-  const int R0 = 2 * c, R1 = 2 * c + 1;
-  const int voff0 = V_OFF + R0 * 128 + ((r ^ (R0 & 7)) << 4);        // tokens 2c,2c+1 ; d [8r, 8r+8)
-  const int voff1 = V_OFF + R1 * 128 + ((r ^ (R1 & 7)) << 4);        // d [64+8r, 64+8r+8)
-  const int voff2 = V_OFF + (R0 + 8) * 128 + ((r ^ (R0 & 7)) << 4);  // tokens 8+2c, 9+2c
-  const int voff3 = V_OFF + (R1 + 8) * 128 + ((r ^ (R1 & 7)) << 4);
+  // Per-thread smem offsets inside a page, as bases plus immediates.  K unit i
+  // of row pair r = {K[r][16c+4i..], K[r+8][16c+4i..], K[r][64+16c+4i..],
+  // K[r+8][64+16c+4i..]} sits at r*256 + 16c + 64*(i ^ (r & 1)) (the XOR is the
+  // bank swizzle; every lane must read the same unit per k-step, since the MMA
+  // shares the Q^T fragment across rows), so units 0, 2 are kb02 + {0, 128}
+  // and units 1, 3 are kb13 + {0, 128}.  V: tokens 2c, 2c+1 at vb0 (d [8r, 8r+8))
+  // / vb1 (d [64+8r, ..)); tokens 8+2c, 9+2c 1024 bytes further.
+  const uint32_t kb02 = r * 256 + 16 * c + 64 * (r & 1);
+  const uint32_t kb13 = r * 256 + 16 * c + 64 * ((r & 1) ^ 1);
+  const uint32_t vb0 = V_OFF + (2 * c) * 128 + ((r ^ (2 * c)) << 4);
+  const uint32_t vb1 = V_OFF + (2 * c + 1) * 128 + ((r ^ (2 * c + 1)) << 4);
+  const uint32_t sb = 4 * r;
+  const uint32_t ring_s = smem_u32(ps.ring);
 
   // O^T accumulators: o[nt][mt] : c0 = (d = DA, head 2c), c1 = (DA, 2c+1),
   // c2 = (DA+1, 2c), c3 = (DA+1, 2c+1); DA = (mt < 4 ? 8r + 2mt : 64 + 8r + 2(mt-4)).
@@ -790,16 +808,18 @@ __device__ __forceinline__ void decode_cta(const DecodeParams& p, uint8_t* smem)
   for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
     for (int i = 0; i < 8; ++i) o[nt][i][0] = o[nt][i][1] = o[nt][i][2] = o[nt][i][3] = 0.0f;
-  // Softmax state for heads 8nt + 2c + e (e = 0, 1); l is this thread's partial sum.
+  // Softmax state for rows 8nt + 2c + e (e = 0, 1); l is this thread's partial sum.
+  // Rows past the GQA group (j >= G) start at m = +inf: their scores come out
+  // as -inf (p = 0) and never trigger a rescale, with no per-score check.
   float m[NT][2], l[NT][2];
   bool hvalid[NT][2];
 #pragma unroll
   for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
     for (int e = 0; e < 2; ++e) {
-      m[nt][e] = -INFINITY;
-      l[nt][e] = 0.0f;
       hvalid[nt][e] = 8 * nt + 2 * c + e < G;
+      m[nt][e] = hvalid[nt][e] ? -INFINITY : INFINITY;
+      l[nt][e] = 0.0f;
     }
   float escale = 1.0f;  // V-scale normaliser 2^E (fp16 range guard for P')
   bool escale_set = false;
@@ -813,24 +833,25 @@ __device__ __forceinline__ void decode_cta(const DecodeParams& p, uint8_t* smem)
 #pragma unroll 1
   for (int j = 0; j < ps.nj; ++j) {
     mbar_wait(&ps.full[slot], phase);
-    const uint8_t* pg = ps.ring + slot * PAGE;
-    const uint4 k0 = lds128(pg + koff0), k1 = lds128(pg + koff1);
-    const uint4 k2 = lds128(pg + koff2), k3 = lds128(pg + koff3);
+    const uint32_t pgs = ring_s + slot * PAGE;
+    const uint4 k0 = lds128_at<0>(pgs + kb02), k2 = lds128_at<128>(pgs + kb02);
+    const uint4 k1 = lds128_at<0>(pgs + kb13), k3 = lds128_at<128>(pgs + kb13);
     uint4 v0, v1, v2, v3;
     if (!HI) {
-      v0 = lds128(pg + voff0), v1 = lds128(pg + voff1);
-      v2 = lds128(pg + voff2), v3 = lds128(pg + voff3);
+      v0 = lds128_at<0>(pgs + vb0), v1 = lds128_at<0>(pgs + vb1);
+      v2 = lds128_at<1024>(pgs + vb0), v3 = lds128_at<1024>(pgs + vb1);
     }
-    float ks_r = lds32f(pg + KS_OFF + 4 * r), ks_r8 = lds32f(pg + KS_OFF + 32 + 4 * r);
-    float vs_r = lds32f(pg + VS_OFF + 4 * r), vs_r8 = lds32f(pg + VS_OFF + 32 + 4 * r);
+    const float ks_r = lds32f_at<KS_OFF>(pgs + sb), ks_r8 = lds32f_at<KS_OFF + 32>(pgs + sb);
+    const float vs_r0 = lds32f_at<VS_OFF>(pgs + sb), vs_r80 = lds32f_at<VS_OFF + 32>(pgs + sb);
 
     // ---- S^T = K . Q^T
-    //   INT8: s8 tensor cores on the raw codes, two Q terms (acc1, acc2), 4 k-steps of 32.
+    //   INT8: s8 tensor cores on the raw codes, two Q terms combined in integer
+    //         (128 acc1 + acc2; the 1/128 lives in qscale), 4 k-steps of 32.
     //   FP8 : codes -> f16 (exact), 8 k-steps of 16; g <= 8 uses two chains for ILP.
     constexpr bool TWO_CHAINS = !HI;
     float st[NT][4];
     {
-      // kr[i] / kr8[i]: 4 codes of token r / r+8 at d = base(i) .. base(i) + 3
+      // kr[i] / kr8[i]: 4 codes of token r / r+8 at k-step i's d range
       const uint32_t kr[8] = {k0.x, k1.x, k2.x, k3.x, k0.z, k1.z, k2.z, k3.z};
       const uint32_t kr8[8] = {k0.y, k1.y, k2.y, k3.y, k0.w, k1.w, k2.w, k3.w};
       uint4 qpair[NT];
@@ -860,14 +881,13 @@ __device__ __forceinline__ void decode_cta(const DecodeParams& p, uint8_t* smem)
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
-          for (int e = 0; e < 4; ++e)
-            st[nt][e] = fmaf(__int2float_rn(acc2[nt][e]), 0.0078125f, __int2float_rn(acc1[nt][e]));
+          for (int e = 0; e < 4; ++e) st[nt][e] = __int2float_rn(acc1[nt][e] * 128 + acc2[nt][e]);
       } else {
-        float sa[NT][4], sb[NT][4];
+        float sa[NT][4], sb2[NT][4];
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
-          for (int e = 0; e < 4; ++e) sa[nt][e] = sb[nt][e] = 0.0f;
+          for (int e = 0; e < 4; ++e) sa[nt][e] = sb2[nt][e] = 0.0f;
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
           uint32_t a0, a2, a1, a3;
@@ -885,142 +905,151 @@ __device__ __forceinline__ void decode_cta(const DecodeParams& p, uint8_t* smem)
               b0 = qf[nt][i][0];
               b1 = qf[nt][i][1];
             }
-            mma16816((TWO_CHAINS && i >= 4) ? sb[nt] : sa[nt], a0, a1, a2, a3, b0, b1);
+            mma16816((TWO_CHAINS && i >= 4) ? sb2[nt] : sa[nt], a0, a1, a2, a3, b0, b1);
           }
         }
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
-          for (int e = 0; e < 4; ++e) st[nt][e] = TWO_CHAINS ? sa[nt][e] + sb[nt][e] : sa[nt][e];
+          for (int e = 0; e < 4; ++e) st[nt][e] = TWO_CHAINS ? sa[nt][e] + sb2[nt][e] : sa[nt][e];
       }
     }
     if (HI) {  // g > 8: load V only after QK^T retired (keeps the live set under 128 regs)
       uint32_t dep;
       asm volatile("mov.b32 %0, 0;" : "=r"(dep) : "f"(st[0][0]), "f"(st[NT - 1][3]));
-      v0 = lds128(pg + voff0 + dep), v1 = lds128(pg + voff1 + dep);
-      v2 = lds128(pg + voff2 + dep), v3 = lds128(pg + voff3 + dep);
+      v0 = lds128_at<0>(pgs + vb0 + dep), v1 = lds128_at<0>(pgs + vb1 + dep);
+      v2 = lds128_at<1024>(pgs + vb0 + dep), v3 = lds128_at<1024>(pgs + vb1 + dep);
     }
-    // ---- scores relative to the running max, log2 units: u = S^T * scale_k * qscale - m
-    //      (one FFMA); thread holds tokens r, r+8 x heads 2c, 2c+1 per n-tile.
     const int tok_base = (pg0 + warp + j * NW) * BS;
-    const bool tail = tok_base + BS > L_all;  // page holds tokens some query row must not see
-    const bool ok_r = !tail || tok_base + r < L, ok_r8 = !tail || tok_base + r + 8 < L;
-    if (!ok_r) vs_r = 0.0f;
-    if (!ok_r8) vs_r8 = 0.0f;
-    const float kq_r = ks_r * qscale, kq_r8 = ks_r8 * qscale;
-    // st[nt]: [0]=(r,2c) [1]=(r,2c+1) [2]=(r+8,2c) [3]=(r+8,2c+1)
-    float u[NT][4];
-    bool over = false;
-#pragma unroll
-    for (int nt = 0; nt < NT; ++nt) {
-#pragma unroll
-      for (int q4 = 0; q4 < 4; ++q4) {
-        const bool ok = !tail || tok_base + (q4 < 2 ? r : r + 8) < vis(nt, q4 & 1);
-        u[nt][q4] = ok ? fmaf(st[nt][q4], q4 < 2 ? kq_r : kq_r8, -m[nt][q4 & 1]) : -INFINITY;
-        over |= hvalid[nt][q4 & 1] && u[nt][q4] > 8.0f;
+
+    // ---- softmax + PV of one page.  TAIL pages (some token past a query row's
+    // visible length) get the masked instantiation; every other page runs the
+    // unmasked one.
+    auto page_tail = [&](auto tail_c) {
+      constexpr bool TAIL = decltype(tail_c)::value;
+      float vs_r = vs_r0, vs_r8 = vs_r80;
+      if (TAIL) {
+        if (tok_base + r >= L) vs_r = 0.0f;
+        if (tok_base + r + 8 >= L) vs_r8 = 0.0f;
       }
-    }
-    // ---- lazy rescale: p = 2^u must stay <= 2^8, and P' = p * scale_v * 2^E must
-    //      stay in f16 range (2^E keeps the page's max V scale in [2^-10, 2^4]).
-    //      Checked per thread + warp votes; the exact maxima (shuffle
-    //      reductions) are only computed on the rare pages that need a rescale.
-    const float ve_r = vs_r * escale, ve_r8 = vs_r8 * escale;
-    const bool trig = __any_sync(FULL, over || !escale_set || ve_r > 16.0f || ve_r8 > 16.0f) ||
-                      (__all_sync(FULL, ve_r < 0.0009765625f && ve_r8 < 0.0009765625f) &&
-                       __any_sync(FULL, vs_r > 0.0f || vs_r8 > 0.0f));
-    if (trig) {
-      float mx[NT][2];
+      const float kq_r = ks_r * qscale, kq_r8 = ks_r8 * qscale;
+      // scores relative to the running max, log2 units: u = S^T * scale_k * qscale - m (one FFMA);
+      // st[nt]: [0]=(r,2c) [1]=(r,2c+1) [2]=(r+8,2c) [3]=(r+8,2c+1)
+      auto visible = [&](int nt, int q4) { return !TAIL || tok_base + (q4 < 2 ? r : r + 8) < vis(nt, q4 & 1); };
+      float u[NT][4];
+      float umax = -INFINITY;
 #pragma unroll
       for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
-        for (int e = 0; e < 2; ++e)
-          mx[nt][e] = fmaxf((!tail || tok_base + r < vis(nt, e)) ? st[nt][e] * kq_r : -INFINITY,
-                            (!tail || tok_base + r + 8 < vis(nt, e)) ? st[nt][e + 2] * kq_r8 : -INFINITY);
-      float vmax = fmaxf(vs_r, vs_r8);
+        for (int q4 = 0; q4 < 4; ++q4) {
+          u[nt][q4] = fmaf(st[nt][q4], q4 < 2 ? kq_r : kq_r8, -m[nt][q4 & 1]);
+          if (TAIL && !visible(nt, q4)) u[nt][q4] = -INFINITY;
+          umax = fmaxf(umax, u[nt][q4]);
+        }
+      // ---- lazy rescale: p = 2^u must stay <= 2^8, and P' = p * scale_v * 2^E must
+      //      stay in f16 range (2^E keeps the page's max V scale in [2^-10, 2^4]).
+      //      Checked per thread + warp votes; the exact maxima (shuffle
+      //      reductions) are only computed on the rare pages that need a rescale.
+      const float ve_r = vs_r * escale, ve_r8 = vs_r8 * escale;
+      const bool trig = __any_sync(FULL, umax > 8.0f || !escale_set || fmaxf(ve_r, ve_r8) > 16.0f) ||
+                        (__all_sync(FULL, fmaxf(ve_r, ve_r8) < 0.0009765625f) &&
+                         __any_sync(FULL, fmaxf(vs_r, vs_r8) > 0.0f));
+      if (trig) {
+        float mx[NT][2];
 #pragma unroll
-      for (int o2 = 4; o2 <= 16; o2 <<= 1) {
+        for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+          for (int e = 0; e < 2; ++e)
+            mx[nt][e] = fmaxf(visible(nt, e) ? st[nt][e] * kq_r : -INFINITY,
+                              visible(nt, e + 2) ? st[nt][e + 2] * kq_r8 : -INFINITY);
+        float vmax = fmaxf(vs_r, vs_r8);
+#pragma unroll
+        for (int o2 = 4; o2 <= 16; o2 <<= 1) {
+#pragma unroll
+          for (int nt = 0; nt < NT; ++nt) {
+            mx[nt][0] = fmaxf(mx[nt][0], __shfl_xor_sync(FULL, mx[nt][0], o2));
+            mx[nt][1] = fmaxf(mx[nt][1], __shfl_xor_sync(FULL, mx[nt][1], o2));
+          }
+          vmax = fmaxf(vmax, __shfl_xor_sync(FULL, vmax, o2));
+        }
+        const float ve = vmax * escale;
+        float e_new = escale;
+        if (vmax > 0.0f && (!escale_set || ve > 16.0f || ve < 0.0009765625f)) {
+          int ex;
+          frexpf(vmax, &ex);
+          e_new = pow2i(-ex);
+          escale_set = true;
+        }
+        const float er = e_new / escale;  // exact power of two
+        escale = e_new;
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt) {
-          mx[nt][0] = fmaxf(mx[nt][0], __shfl_xor_sync(FULL, mx[nt][0], o2));
-          mx[nt][1] = fmaxf(mx[nt][1], __shfl_xor_sync(FULL, mx[nt][1], o2));
+          float f[2];
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const bool nm = mx[nt][e] > m[nt][e] + 8.0f;  // never for rows past G (m = +inf)
+            const float cl = nm ? fast_exp2(m[nt][e] - mx[nt][e]) : 1.0f;
+            if (nm) m[nt][e] = mx[nt][e];
+            l[nt][e] *= cl;
+            f[e] = cl * er;
+          }
+#pragma unroll
+          for (int mt = 0; mt < 8; ++mt) {
+            o[nt][mt][0] *= f[0];
+            o[nt][mt][1] *= f[1];
+            o[nt][mt][2] *= f[0];
+            o[nt][mt][3] *= f[1];
+          }
+#pragma unroll
+          for (int q4 = 0; q4 < 4; ++q4) {
+            u[nt][q4] = fmaf(st[nt][q4], q4 < 2 ? kq_r : kq_r8, -m[nt][q4 & 1]);
+            if (TAIL && !visible(nt, q4)) u[nt][q4] = -INFINITY;
+          }
         }
-        vmax = fmaxf(vmax, __shfl_xor_sync(FULL, vmax, o2));
       }
-      const float ve = vmax * escale;
-      float e_new = escale;
-      if (vmax > 0.0f && (!escale_set || ve > 16.0f || ve < 0.0009765625f)) {
-        int ex;
-        frexpf(vmax, &ex);
-        e_new = pow2i(-ex);
-        escale_set = true;
-      }
-      const float er = e_new / escale;  // exact power of two
-      escale = e_new;
+      // ---- p (fp32, for l) and P' = p * scale_v * 2^E (fp16) -> P'^T B-fragments
+      const float w_r = vs_r * escale, w_r8 = vs_r8 * escale;
+      uint32_t pb[NT][2];
 #pragma unroll
       for (int nt = 0; nt < NT; ++nt) {
-        float f[2];
-#pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const bool nm = hvalid[nt][e] && mx[nt][e] > m[nt][e] + 8.0f;
-          const float cl = nm ? fast_exp2(m[nt][e] - mx[nt][e]) : 1.0f;
-          if (nm) m[nt][e] = mx[nt][e];
-          l[nt][e] *= cl;
-          f[e] = cl * er;
-        }
-#pragma unroll
-        for (int mt = 0; mt < 8; ++mt) {
-          o[nt][mt][0] *= f[0];
-          o[nt][mt][1] *= f[1];
-          o[nt][mt][2] *= f[0];
-          o[nt][mt][3] *= f[1];
-        }
+        float pv[4];
 #pragma unroll
         for (int q4 = 0; q4 < 4; ++q4) {
-          const bool ok = !tail || tok_base + (q4 < 2 ? r : r + 8) < vis(nt, q4 & 1);
-          u[nt][q4] = ok ? fmaf(st[nt][q4], q4 < 2 ? kq_r : kq_r8, -m[nt][q4 & 1]) : -INFINITY;
+          pv[q4] = fast_exp2(u[nt][q4]);
+          l[nt][q4 & 1] += pv[q4];
         }
+        // 8x8 blocks: rows = tokens (r | r+8), cols = heads (2c, 2c+1)
+        const uint32_t x0 = pack_half2(pv[0] * w_r, pv[1] * w_r);
+        const uint32_t x1 = pack_half2(pv[2] * w_r8, pv[3] * w_r8);
+        pb[nt][0] = movmatrix_trans(x0);  // (tokens 2c, 2c+1 ; head r)
+        pb[nt][1] = movmatrix_trans(x1);  // (tokens 8+2c, 9+2c ; head r)
       }
-    }
-    // ---- p (fp32, for l) and P' = p * scale_v * 2^E (fp16) -> P'^T B-fragments
-    const float w_r = vs_r * escale, w_r8 = vs_r8 * escale;
-    uint32_t pb[NT][2];
-#pragma unroll
-    for (int nt = 0; nt < NT; ++nt) {
-      float pv[4];
-#pragma unroll
-      for (int q4 = 0; q4 < 4; ++q4) {
-        const int e = q4 & 1;
-        pv[q4] = hvalid[nt][e] ? fast_exp2(u[nt][q4]) : 0.0f;
-        l[nt][e] += pv[q4];
-      }
-      // 8x8 blocks: rows = tokens (r | r+8), cols = heads (2c, 2c+1)
-      const uint32_t x0 = pack_half2(pv[0] * w_r, pv[1] * w_r);
-      const uint32_t x1 = pack_half2(pv[2] * w_r8, pv[3] * w_r8);
-      pb[nt][0] = movmatrix_trans(x0);  // (tokens 2c, 2c+1 ; head r)
-      pb[nt][1] = movmatrix_trans(x1);  // (tokens 8+2c, 9+2c ; head r)
-    }
-    // ---- O^T += V^T . P'^T
-    const uint32_t va[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};  // tokens 2c, 2c+1
-    const uint32_t vb[8] = {v2.x, v2.y, v2.z, v2.w, v3.x, v3.y, v3.z, v3.w};  // tokens 8+2c, 9+2c
-    uint32_t vmask_a = 0xffffffffu, vmask_b = 0xffffffffu;
-    if (KVD == KVQ_FP8_E4M3 && tail) {  // garbage E4M3 codes may be NaN: zero masked tokens
-      vmask_a = (tok_base + 2 * c < L ? 0x0000ffffu : 0u) | (tok_base + 2 * c + 1 < L ? 0xffff0000u : 0u);
-      vmask_b = (tok_base + 8 + 2 * c < L ? 0x0000ffffu : 0u) | (tok_base + 9 + 2 * c < L ? 0xffff0000u : 0u);
-    }
-#pragma unroll
-    for (int mt = 0; mt < 8; ++mt) {
-      uint32_t a0, a1, a2, a3;
-      codes_to_f16x2<KVD>(va[mt], a0, a1);  // (DA, tok 2c|2c+1), (DA+1, ...)
-      codes_to_f16x2<KVD>(vb[mt], a2, a3);  // (DA, tok 8+2c|9+2c), (DA+1, ...)
-      if (KVD == KVQ_FP8_E4M3) {
-        a0 &= vmask_a;
-        a1 &= vmask_a;
-        a2 &= vmask_b;
-        a3 &= vmask_b;
+      // ---- O^T += V^T . P'^T
+      const uint32_t va[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};  // tokens 2c, 2c+1
+      const uint32_t vbw[8] = {v2.x, v2.y, v2.z, v2.w, v3.x, v3.y, v3.z, v3.w};  // tokens 8+2c, 9+2c
+      uint32_t vmask_a = 0xffffffffu, vmask_b = 0xffffffffu;
+      if (KVD == KVQ_FP8_E4M3 && TAIL) {  // garbage E4M3 codes may be NaN: zero masked tokens
+        vmask_a = (tok_base + 2 * c < L ? 0x0000ffffu : 0u) | (tok_base + 2 * c + 1 < L ? 0xffff0000u : 0u);
+        vmask_b = (tok_base + 8 + 2 * c < L ? 0x0000ffffu : 0u) | (tok_base + 9 + 2 * c < L ? 0xffff0000u : 0u);
       }
 #pragma unroll
-      for (int nt = 0; nt < NT; ++nt) mma16816(o[nt][mt], a0, a1, a2, a3, pb[nt][0], pb[nt][1]);
-    }
+      for (int mt = 0; mt < 8; ++mt) {
+        uint32_t a0, a1, a2, a3;
+        codes_to_f16x2<KVD>(va[mt], a0, a1);   // (DA, tok 2c|2c+1), (DA+1, ...)
+        codes_to_f16x2<KVD>(vbw[mt], a2, a3);  // (DA, tok 8+2c|9+2c), (DA+1, ...)
+        if (KVD == KVQ_FP8_E4M3 && TAIL) {
+          a0 &= vmask_a;
+          a1 &= vmask_a;
+          a2 &= vmask_b;
+          a3 &= vmask_b;
+        }
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) mma16816(o[nt][mt], a0, a1, a2, a3, pb[nt][0], pb[nt][1]);
+      }
+    };
+    if (tok_base + BS > L_all) page_tail(std::true_type{});
+    else page_tail(std::false_type{});
+
     // ---- refill this slot with page j + S.  Every LDS of the slot has
     // returned (its registers were consumed by the MMAs above) in every lane
     // (__syncwarp), so the async-proxy overwrite cannot race the reads.

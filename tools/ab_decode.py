@@ -1,0 +1,85 @@
+"""A/B timing of kvq_decode_attn across libkvq builds (any ABI version that
+exports kvq_decode_attn / kvq_decode_pages_per_split / workspace_bytes).
+
+    python tools/ab_decode.py CONFIG lib1.so [lib2.so ...]
+
+CONFIG is one of c2, c3, c4 (bench.py shapes).  Pages are random codes with
+fixed positive scales (timing only); block ids are a random permutation.
+Each lib is timed in alternation (5 rounds x 20 launches, CUDA events), so
+box-level drift affects every build alike.
+"""
+import ctypes
+import sys
+
+import numpy as np
+import torch
+
+SHAPES = {"c2": (256, 32, 8, "ragged", 0), "c3": (128, 64, 8, 32768, 1), "c4": (64, 64, 4, 131072, 0)}
+
+
+def main():
+    cfg, libs = sys.argv[1], sys.argv[2:]
+    B, Hq, Hkv, ctx, kvd = SHAPES[cfg]
+    lens = (np.random.default_rng(3).integers(512, 8193, size=B) if ctx == "ragged"
+            else np.full(B, ctx)).astype(np.int64) + 1
+    nblk = -(-lens // 16)
+    NB, mb = int(nblk.sum()), int(nblk.max())
+    dev = torch.device("cuda:0")
+    pool = torch.randint(0, 256, (NB, Hkv, 4224), dtype=torch.uint8, device=dev)
+    if kvd == 1:
+        pool[..., :4096] &= 0xF7  # no NaN E4M3 codes
+    sc = torch.full((NB, Hkv, 32), 0.02, dtype=torch.float32, device=dev)
+    pool[..., 4096:] = sc.view(torch.uint8).view(NB, Hkv, 128)
+    perm = np.random.default_rng(7).permutation(NB).astype(np.int32)
+    table = np.zeros((B, mb), np.int32)
+    pos = 0
+    for b in range(B):
+        table[b, : nblk[b]] = perm[pos: pos + nblk[b]]
+        pos += nblk[b]
+    table = torch.from_numpy(table).to(dev)
+    seq = torch.from_numpy(lens.astype(np.int32)).to(dev)
+    q = torch.randn((B, Hq, 128), device=dev).to(torch.bfloat16)
+    out = torch.empty((Hq, B, 128), dtype=torch.bfloat16, device=dev)
+    stream = torch.cuda.current_stream().cuda_stream
+    runs = []
+    for path in libs:
+        L = ctypes.CDLL(path)
+        L.kvq_decode_pages_per_split.restype = ctypes.c_int32
+        L.kvq_decode_pages_per_split.argtypes = [ctypes.c_int32, ctypes.c_int32, ctypes.c_int64, ctypes.c_int32]
+        L.kvq_decode_workspace_bytes.restype = ctypes.c_size_t
+        L.kvq_decode_workspace_bytes.argtypes = [ctypes.c_int32] * 4
+        vp, i32, i64 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64
+        L.kvq_decode_attn.argtypes = [vp, i64, vp, i64, vp, i32, vp, i32, i32, i32, i32, ctypes.c_float, i32,
+                                      vp, ctypes.c_size_t, vp, i32, i32, vp]
+        pps = L.kvq_decode_pages_per_split(B, Hkv, NB, mb)
+        wsb = L.kvq_decode_workspace_bytes(B, Hq, Hkv, -(-mb // pps))
+        ws = torch.zeros(wsb, dtype=torch.uint8, device=dev)
+
+        def launch(L=L, pps=pps, ws=ws, wsb=wsb):
+            st = L.kvq_decode_attn(q.data_ptr(), q.stride(0), pool.data_ptr(), NB, table.data_ptr(), mb,
+                                   seq.data_ptr(), B, Hq, Hkv, kvd, 0.0884, pps, ws.data_ptr(), wsb,
+                                   out.data_ptr(), 0, 1, stream)
+            assert st == 0, st
+        launch()
+        runs.append((path, launch, []))
+    torch.cuda.synchronize()
+    for _ in range(5):
+        for path, launch, times in runs:
+            for _ in range(3):
+                launch()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for _ in range(20):
+                launch()
+            e1.record()
+            torch.cuda.synchronize()
+            times.append(e0.elapsed_time(e1) / 20)
+    byt = int(lens.sum()) * Hkv * 264 + B * Hq * 512 + int(nblk.sum()) * 4
+    for path, _, times in runs:
+        t = min(times)
+        print(f"{cfg} {path}: min {t * 1e3:.1f} us  median {sorted(times)[2] * 1e3:.1f} us  "
+              f"{byt / t / 1e6:.0f} GB/s")
+
+
+if __name__ == "__main__":
+    main()

@@ -354,14 +354,15 @@ def run_ours(args, cfg):
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g):
             for i in range(n):
-                sess.k1(buf)
-                if timed and i % k2_every == 0:
+                if timed and i % k2_every == 0:  # sampled step: K1, event, K2, event
+                    sess.k1(buf)
                     evs[i] = (torch.cuda.Event(enable_timing=True, external=True),
                               torch.cuda.Event(enable_timing=True, external=True))
                     evs[i][0].record()
-                sess.k2(buf)
-                if i in evs:
+                    sess.k2(buf)
                     evs[i][1].record()
+                else:                            # kvq_decode_step: K2 PDL-launched behind K1
+                    sess.step(buf)
                 if gather_in_graph:
                     gather_dev(buf["out"])
         return g, list(evs.values())
@@ -500,9 +501,10 @@ def run_ours(args, cfg):
                    if world > 1 else "1 GPU",
                    "l2": "inputs larger than L2 (pool %.2f GB vs 126 MB L2); no flush" % (cache.nbytes() * world / 1e9)
                    if cache.nbytes() * world > 4 * 126e6 else "pool fits in L2: L2-resident numbers",
-                   "step": "K1 append of B rows + K2 paged decode attention (+ all-gather if N>1); "
-                           "stationary ctx; the K timed steps are one CUDA graph (K1, K2 per step, unrolled); "
-                           "K2 launch time from event nodes around every k2_sample_every-th K2",
+                   "step": "K1 append of B rows + K2 paged decode attention (+ the gather if N>1); "
+                           "stationary ctx; the K timed steps are one CUDA graph (kvq_decode_step per step: K2 "
+                           "launched behind K1 with programmatic dependent launch, unrolled); K2 launch time "
+                           "from event nodes around every k2_sample_every-th K2 (those steps launch K1, K2 plainly)",
                    "e2e": "DecodeSession(graphs=True).submit_staged: one H2D of the pinned q/k/v/slots/lens "
                           "staging blob, graph of K1, K2 (, all-gather), D2H of O; double-buffered copy "
                           "streams overlap adjacent steps",

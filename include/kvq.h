@@ -162,6 +162,51 @@ int kvq_decode_attn_peer(const void* q, int64_t q_batch_stride, const void* pool
                          int32_t pages_per_split, void* workspace, size_t workspace_bytes,
                          const kvq_peer_out* peer, void* stream);
 
+/* One decode step in one call: kvq_quant_append of the T new rows, then
+ * kvq_decode_attn (or, with `peer`, kvq_decode_attn_peer; `out` is then
+ * ignored and must be bf16 head-major).  K2 is launched with programmatic
+ * stream serialization right behind K1 (PDL): its launch and prologue (q,
+ * block-table and barrier setup) overlap K1, and it waits for K1
+ * (griddepcontrol.wait) before reading any page.  Valid because K1 writes
+ * only pages; q, block_table and seq_lens must be ready when the call is
+ * enqueued, as for any stream-ordered call.  Replaces the decode-step pair
+ * the reference charges as one constant, simulator.py:499-517. */
+int kvq_decode_step(const void* k, const void* v, int64_t k_token_stride, int64_t v_token_stride,
+                    const int32_t* slot_mapping, int32_t T, const void* q, int64_t q_batch_stride,
+                    void* pool, int64_t num_blocks, const int32_t* block_table, int32_t max_blocks,
+                    const int32_t* seq_lens, int32_t B, int32_t Hq, int32_t Hkv, int32_t kv_dtype,
+                    float sm_scale, int32_t pages_per_split, void* workspace, size_t workspace_bytes,
+                    void* out, int32_t out_dtype, int32_t out_layout, const kvq_peer_out* peer,
+                    void* stream);
+
+/* Host-side step submission of a double-buffered serving pipeline, in one
+ * native call instead of ~10 runtime calls from the host language: upload the
+ * step's packed inputs (pinned host -> device) on `h2d_stream`, run the slot's
+ * captured device step (a cudaGraphExec_t holding kvq_decode_step and, when
+ * sharded, the gather) on `compute_stream`, download the output on
+ * `d2h_stream`, with the three events ordering slot reuse (the caller creates
+ * them; `reuse` = the slot ran before).  The session runtime behind
+ * DecodeSession.submit_staged; replaces the per-step host work of the
+ * reference's decode loop, simulator.py:499-517. */
+typedef struct kvq_pipe_step {
+  void* h2d_stream;
+  void* compute_stream;
+  void* d2h_stream;
+  void* graph_exec;
+  void* dev_in;
+  const void* host_in;
+  size_t in_bytes;
+  const void* dev_out;
+  void* host_out;
+  size_t out_bytes;
+  void* ev_in_ready;
+  void* ev_done;
+  void* ev_out_done;
+  int32_t reuse;
+  int32_t reserved;
+} kvq_pipe_step;
+int kvq_pipeline_submit(const kvq_pipe_step* step);
+
 /* Symmetric-buffer plumbing (setup time only, not on the step path):
  * allocate `bytes` of zeroed device memory on the current device and return
  * its IPC handle; map a peer's handle into this process; unmap; free. */

@@ -40,6 +40,9 @@ SIGNATURES = {
     "kvq_block_hashes": (_i64, [_vp, _i64, _i32, _c.c_uint64, _vp]),
     "kvq_decode_attn_peer": (_c.c_int, [_vp, _i64, _vp, _i64, _vp, _i32, _vp, _i32, _i32, _i32, _i32,
                                         _f32, _i32, _vp, _sz, _vp, _vp]),
+    "kvq_decode_step": (_c.c_int, [_vp, _vp, _i64, _i64, _vp, _i32, _vp, _i64, _vp, _i64, _vp, _i32, _vp,
+                                   _i32, _i32, _i32, _i32, _f32, _i32, _vp, _sz, _vp, _i32, _i32, _vp, _vp]),
+    "kvq_pipeline_submit": (_c.c_int, [_vp]),
     "kvq_sym_alloc": (_c.c_int, [_sz, _c.POINTER(_vp), _vp]),
     "kvq_sym_open": (_c.c_int, [_vp, _c.POINTER(_vp)]),
     "kvq_sym_close": (_c.c_int, [_vp]),
@@ -49,6 +52,14 @@ SIGNATURES = {
 MAX_PEERS = 8
 PEER_CTL_BYTES = 256
 IPC_HANDLE_BYTES = 64
+
+
+class PipeStep(_c.Structure):
+    """``kvq_pipe_step`` (include/kvq.h): one slot of the native step submitter."""
+    _fields_ = [("h2d_stream", _vp), ("compute_stream", _vp), ("d2h_stream", _vp), ("graph_exec", _vp),
+                ("dev_in", _vp), ("host_in", _vp), ("in_bytes", _sz), ("dev_out", _vp), ("host_out", _vp),
+                ("out_bytes", _sz), ("ev_in_ready", _vp), ("ev_done", _vp), ("ev_out_done", _vp),
+                ("reuse", _i32), ("reserved", _i32)]
 
 
 class PeerOutDesc(_c.Structure):

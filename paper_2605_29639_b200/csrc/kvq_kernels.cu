@@ -114,6 +114,9 @@ __global__ void __launch_bounds__(K1_THREADS) quant_append_kernel(
     const __nv_bfloat16* __restrict__ k, const __nv_bfloat16* __restrict__ v, int64_t k_stride,
     int64_t v_stride, const int32_t* __restrict__ slots, int T, int Hkv,
     uint8_t* __restrict__ pool, int64_t num_blocks) {
+  // A K2 launched behind this kernel with programmatic serialization may start
+  // its prologue now; it waits (griddepcontrol.wait) before reading any page.
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   __shared__ __align__(16) uint8_t img[K1_HEADS][PAGE];
   const int t0 = blockIdx.x * 16, h0 = blockIdx.y * K1_HEADS;
   const int grp = threadIdx.x >> 3, j = threadIdx.x & 7;  // lane j of the group owns d [16j, 16j+16)
@@ -243,6 +246,9 @@ __global__ void __launch_bounds__(K1R_WARPS * 32) quant_append_rows_kernel(
     const __nv_bfloat16* __restrict__ k, const __nv_bfloat16* __restrict__ v, int64_t k_stride,
     int64_t v_stride, const int32_t* __restrict__ slots, int T, int Hkv,
     uint8_t* __restrict__ pool, int64_t num_blocks) {
+  // A K2 launched behind this kernel with programmatic serialization may start
+  // its prologue now; it waits (griddepcontrol.wait) before reading any page.
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const int row = blockIdx.x * K1R_WARPS + (threadIdx.x >> 5);  // t * Hkv + h
   const int lane = threadIdx.x & 31;
   if (row >= T * Hkv) return;  // whole warps only
@@ -696,6 +702,10 @@ __device__ __forceinline__ void decode_cta(const DecodeParams& p, uint8_t* smem)
   }
   __syncwarp();
   ps.init(lane);
+  // Launched behind K1 with programmatic serialization (kvq_decode_step): the
+  // prologue above (q, block table, barriers) overlapped K1; pages may hold
+  // K1's rows, so wait for it here.  A no-op for an ordinary launch.
+  asm volatile("griddepcontrol.wait;" ::: "memory");
 #pragma unroll 1
   for (int j = 0; j < S && j < ps.nj; ++j) ps.issue(j, lane, j);
 
@@ -1143,10 +1153,10 @@ __device__ __forceinline__ void decode_cta(const DecodeParams& p, uint8_t* smem)
   }
 
   // ===== fused split-KV combine: the last CTA of (b, h) merges all splits =====
-  // Every thread fences its partial stores at gpu scope before the barrier;
-  // thread 0's acq_rel atomic then publishes the split, and the last
-  // arriver's acquire + bar.sync make every split's partials visible.
-  __threadfence();
+  // bar.sync orders every thread's partial stores before thread 0's gpu-scope
+  // acq_rel atomic (its release is cumulative), which publishes the split; the
+  // last arriver's acquire + bar.sync make every split's partials visible.  No
+  // per-thread fence.
   __syncthreads();
   if (tid == 0) {
     int* ctr = p.counters + (int64_t)b * p.Hkv + h;
@@ -1340,7 +1350,7 @@ static int decode_attn_impl(const void* q, int64_t q_batch_stride, int32_t q_len
                             const int32_t* seq_lens, int32_t B, int32_t Hq, int32_t Hkv, int32_t kv_dtype,
                             float sm_scale, int32_t pages_per_split, void* workspace,
                             size_t workspace_bytes, void* out, int32_t out_dtype, int32_t out_layout,
-                            const kvq_peer_out* peer, void* stream) {
+                            const kvq_peer_out* peer, void* stream, bool pdl = false) {
   if (B < 0 || Hq <= 0 || Hkv <= 0 || max_blocks <= 0 || num_blocks <= 0 || q_len <= 0)
     return fail(KVQ_EINVAL, "decode_attn: bad sizes");
   if (B == 0) return KVQ_OK;
@@ -1405,7 +1415,18 @@ static int decode_attn_impl(const void* q, int64_t q_batch_stride, int32_t q_len
       e = cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
                                cudaSharedmemCarveoutMaxShared);
     if (e != cudaSuccess) return fail(KVQ_ECUDA, cudaGetErrorString(e));
-    kernel<<<grid, kvq::THREADS, smem_bytes, st>>>(prm);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = dim3(kvq::THREADS);
+    cfg.dynamicSmemBytes = smem_bytes;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl ? 1 : 0;
+    e = cudaLaunchKernelEx(&cfg, kernel, prm);
+    if (e != cudaSuccess) return fail(KVQ_ECUDA, cudaGetErrorString(e));
     return check_launch("decode_attn");
   };
   const int mode = peer ? 2 : (q_len > 1 ? 1 : 0);
@@ -1419,6 +1440,35 @@ static int decode_attn_impl(const void* q, int64_t q_batch_stride, int32_t q_len
   if (mode == 1)
     return hi ? launch(kvq::decode_kernel<KVQ_FP8_E4M3, true, 1>) : launch(kvq::decode_kernel<KVQ_FP8_E4M3, false, 1>);
   return hi ? launch(kvq::decode_kernel<KVQ_FP8_E4M3, true, 0>) : launch(kvq::decode_kernel<KVQ_FP8_E4M3, false, 0>);
+}
+
+int kvq_decode_step(const void* k, const void* v, int64_t k_token_stride, int64_t v_token_stride,
+                    const int32_t* slot_mapping, int32_t T, const void* q, int64_t q_batch_stride,
+                    void* pool, int64_t num_blocks, const int32_t* block_table, int32_t max_blocks,
+                    const int32_t* seq_lens, int32_t B, int32_t Hq, int32_t Hkv, int32_t kv_dtype,
+                    float sm_scale, int32_t pages_per_split, void* workspace, size_t workspace_bytes,
+                    void* out, int32_t out_dtype, int32_t out_layout, const kvq_peer_out* peer,
+                    void* stream) {
+  if (peer && (out_dtype != KVQ_OUT_BF16 || out_layout != KVQ_OUT_HBD))
+    return fail(KVQ_EINVAL, "decode_step: the fused gather writes bf16 head-major rows");
+  if (int rc = kvq_quant_append(k, v, k_token_stride, v_token_stride, slot_mapping, T, Hkv, kv_dtype, pool,
+                                num_blocks, stream))
+    return rc;
+  if (peer) {
+    const int P = peer->n_peers;
+    if (P < 2 || P > KVQ_MAX_PEERS || peer->rank < 0 || peer->rank >= P || peer->head_offset < 0 ||
+        peer->batch_global < B || peer->writers_per_use == 0)
+      return fail(KVQ_EINVAL, "decode_step: bad peer descriptor");
+    for (int r = 0; r < P; ++r)
+      if (!peer->out[r] || !peer->ctl[r] || !aligned(peer->out[r], 16) || !aligned(peer->ctl[r], 128))
+        return fail(KVQ_EINVAL, "decode_step: peer out (16 B) / ctl (128 B) pointers missing or misaligned");
+    out = peer->out[peer->rank];
+  }
+  // K2 is launched with programmatic stream serialization right behind K1, so
+  // its launch and prologue overlap K1 (K1 never writes q, the table or lens).
+  return decode_attn_impl(q, q_batch_stride, 1, pool, num_blocks, block_table, max_blocks, seq_lens, B, Hq,
+                          Hkv, kv_dtype, sm_scale, pages_per_split, workspace, workspace_bytes, out, out_dtype,
+                          out_layout, peer, stream, /*pdl=*/T > 0);
 }
 
 int kvq_decode_attn_mq(const void* q, int64_t q_batch_stride, int32_t q_len, const void* pool,
@@ -1450,6 +1500,32 @@ int kvq_decode_attn_peer(const void* q, int64_t q_batch_stride, const void* pool
   return decode_attn_impl(q, q_batch_stride, 1, pool, num_blocks, block_table, max_blocks, seq_lens, B, Hq,
                           Hkv, kv_dtype, sm_scale, pages_per_split, workspace, workspace_bytes,
                           peer->out[peer->rank], KVQ_OUT_BF16, KVQ_OUT_HBD, peer, stream);
+}
+
+int kvq_pipeline_submit(const kvq_pipe_step* s) {
+  if (!s || !s->graph_exec || !s->dev_in || !s->host_in || !s->dev_out || !s->host_out || !s->ev_in_ready ||
+      !s->ev_done || !s->ev_out_done)
+    return fail(KVQ_EINVAL, "pipeline_submit: null handle or buffer");
+  auto h2d = static_cast<cudaStream_t>(s->h2d_stream);
+  auto cmp = static_cast<cudaStream_t>(s->compute_stream);
+  auto d2h = static_cast<cudaStream_t>(s->d2h_stream);
+  auto in_ready = static_cast<cudaEvent_t>(s->ev_in_ready);
+  auto done = static_cast<cudaEvent_t>(s->ev_done);
+  auto out_done = static_cast<cudaEvent_t>(s->ev_out_done);
+  cudaError_t e = cudaSuccess;
+  auto ok = [&](cudaError_t r) { if (e == cudaSuccess) e = r; };
+  if (s->reuse) ok(cudaStreamWaitEvent(h2d, done, 0));      // the slot's previous kernels read dev_in
+  ok(cudaMemcpyAsync(s->dev_in, s->host_in, s->in_bytes, cudaMemcpyHostToDevice, h2d));
+  ok(cudaEventRecord(in_ready, h2d));
+  ok(cudaStreamWaitEvent(cmp, in_ready, 0));
+  if (s->reuse) ok(cudaStreamWaitEvent(cmp, out_done, 0));  // the slot's previous download read dev_out
+  ok(cudaGraphLaunch(static_cast<cudaGraphExec_t>(s->graph_exec), cmp));
+  ok(cudaEventRecord(done, cmp));
+  ok(cudaStreamWaitEvent(d2h, done, 0));
+  ok(cudaMemcpyAsync(s->host_out, s->dev_out, s->out_bytes, cudaMemcpyDeviceToHost, d2h));
+  ok(cudaEventRecord(out_done, d2h));
+  if (e != cudaSuccess) return fail(KVQ_ECUDA, cudaGetErrorString(e));
+  return KVQ_OK;
 }
 
 int kvq_sym_alloc(size_t bytes, void** ptr, void* ipc_handle) {

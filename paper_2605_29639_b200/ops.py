@@ -6,6 +6,7 @@ on a CUDA device, or a missing library, raises.
 * :func:`paged_decode_attention` -> ``kvq_decode_attn``  (K2 + fused combine)
 * :func:`paged_decode_attention_gathered` -> ``kvq_decode_attn_peer`` (K2 with
   the KV-head output all-gather fused in, over peer memory)
+* :func:`decode_step`            -> ``kvq_decode_step``  (K1 + K2 in one call, PDL-overlapped)
 * :func:`copy_blocks`            -> ``kvq_copy_blocks``  (copy-on-write pages)
 """
 from __future__ import annotations
@@ -32,6 +33,21 @@ def _require_cuda(name: str, *ts: torch.Tensor) -> None:
             raise ValueError(f"{name}: tensors must be on a CUDA device (no CPU fallback)")
 
 
+def _check_append(fn: str, cache: PagedKVCache, k: torch.Tensor, v: torch.Tensor,
+                  slot_mapping: torch.Tensor) -> None:
+    _require_cuda(fn, k, v, slot_mapping, cache.pool)
+    spec = cache.spec
+    for name, t in (("k", k), ("v", v)):
+        if t.dtype != torch.bfloat16 or t.dim() != 3 or t.shape[1:] != (spec.num_kv_heads, 128):
+            raise ValueError(f"{fn}: {name} must be bf16 [T, {spec.num_kv_heads}, 128]")
+        if t.stride(2) != 1 or t.stride(1) != 128:
+            raise ValueError(f"{fn}: {name} heads must be contiguous")
+    if k.shape[0] != v.shape[0] or slot_mapping.shape != (k.shape[0],):
+        raise ValueError(f"{fn}: T mismatch")
+    if slot_mapping.dtype != torch.int32 or not slot_mapping.is_contiguous():
+        raise ValueError(f"{fn}: slot_mapping must be contiguous int32")
+
+
 def quantize_append(cache: PagedKVCache, k: torch.Tensor, v: torch.Tensor,
                     slot_mapping: torch.Tensor) -> None:
     """Quantize new K/V rows and scatter them into their pages.
@@ -39,17 +55,8 @@ def quantize_append(cache: PagedKVCache, k: torch.Tensor, v: torch.Tensor,
     k, v: bf16 ``[T, Hkv, 128]`` (token stride may exceed ``Hkv*128``, e.g.
     slices of a fused QKV buffer); slot_mapping: int32 ``[T]`` with
     ``block * 16 + offset`` (negative = skip)."""
-    _require_cuda("quantize_append", k, v, slot_mapping, cache.pool)
+    _check_append("quantize_append", cache, k, v, slot_mapping)
     spec = cache.spec
-    for name, t in (("k", k), ("v", v)):
-        if t.dtype != torch.bfloat16 or t.dim() != 3 or t.shape[1:] != (spec.num_kv_heads, 128):
-            raise ValueError(f"quantize_append: {name} must be bf16 [T, {spec.num_kv_heads}, 128]")
-        if t.stride(2) != 1 or t.stride(1) != 128:
-            raise ValueError(f"quantize_append: {name} heads must be contiguous")
-    if k.shape[0] != v.shape[0] or slot_mapping.shape != (k.shape[0],):
-        raise ValueError("quantize_append: T mismatch")
-    if slot_mapping.dtype != torch.int32 or not slot_mapping.is_contiguous():
-        raise ValueError("quantize_append: slot_mapping must be contiguous int32")
     lib = _lib.load()
     st = lib.kvq_quant_append(k.data_ptr(), v.data_ptr(), k.stride(0), v.stride(0),
                               slot_mapping.data_ptr(), k.shape[0], spec.num_kv_heads,
@@ -200,6 +207,67 @@ def paged_decode_attention_gathered(q: torch.Tensor, cache: PagedKVCache, block_
         ctypes.addressof(peer.descs[slot]), _stream_handle(q.device))
     _lib.check("kvq_decode_attn_peer", st)
     return peer.out(slot)
+
+
+def decode_step(cache: PagedKVCache, k: torch.Tensor, v: torch.Tensor, slot_mapping: torch.Tensor,
+                q: torch.Tensor, block_table: torch.Tensor, seq_lens: torch.Tensor, *,
+                sm_scale: Optional[float] = None, pages_per_split: Optional[int] = None,
+                total_pages: Optional[int] = None, out: Optional[torch.Tensor] = None,
+                out_dtype: torch.dtype = torch.bfloat16, head_major: bool = False,
+                workspace: Optional[torch.Tensor] = None, peer=None, slot: int = 0) -> torch.Tensor:
+    """One decode step in one call (``kvq_decode_step``): :func:`quantize_append`
+    of the new rows, then :func:`paged_decode_attention` (or, with ``peer``,
+    :func:`paged_decode_attention_gathered`), with K2 launched behind K1 by
+    programmatic dependent launch so its launch and prologue overlap K1.
+    Same arguments and results as the two calls in sequence."""
+    _check_append("decode_step", cache, k, v, slot_mapping)
+    _require_cuda("decode_step", q, block_table, seq_lens)
+    spec = cache.spec
+    if q.dtype != torch.bfloat16 or q.dim() != 3 or q.shape[-1] != 128 or q.stride(-1) != 1 \
+            or q.stride(-2) != 128:
+        raise ValueError("decode_step: q must be bf16 [B, Hq, 128] with contiguous heads")
+    B, Hq = q.shape[0], q.shape[1]
+    if block_table.dtype != torch.int32 or block_table.dim() != 2 or block_table.shape[0] != B \
+            or not block_table.is_contiguous():
+        raise ValueError("decode_step: block_table must be contiguous int32 [B, max_blocks]")
+    if seq_lens.dtype != torch.int32 or seq_lens.shape != (B,) or not seq_lens.is_contiguous():
+        raise ValueError("decode_step: seq_lens must be contiguous int32 [B]")
+    import ctypes
+    desc = None
+    if peer is not None:
+        if not 0 <= slot < peer.slots or peer.plan.q_range[1] - peer.plan.q_range[0] != Hq:
+            raise ValueError("decode_step: bad slot, or q heads do not match the shard plan")
+        out, out_dtype, head_major = peer.out(slot), torch.bfloat16, True
+        desc = ctypes.addressof(peer.descs[slot])
+    else:
+        shape = (Hq, B, 128) if head_major else (B, Hq, 128)
+        if out is None:
+            out = torch.empty(shape, dtype=out_dtype, device=q.device)
+        elif tuple(out.shape) != shape or out.dtype != out_dtype or not out.is_contiguous():
+            raise ValueError(f"decode_step: out must be contiguous {out_dtype} {shape}")
+        if out_dtype not in (torch.bfloat16, torch.float32):
+            raise ValueError("decode_step: out_dtype must be bf16 or fp32")
+    if sm_scale is None:
+        sm_scale = 1.0 / math.sqrt(128)
+    lib = _lib.load()
+    max_blocks = block_table.shape[1]
+    pps = pages_per_split or lib.kvq_decode_pages_per_split(
+        B, spec.num_kv_heads, total_pages if total_pages is not None else B * max_blocks, max_blocks)
+    max_splits = -(-max_blocks // pps)
+    nbytes = lib.kvq_decode_workspace_bytes(B, Hq, spec.num_kv_heads, max_splits)
+    if workspace is None:
+        workspace = _workspace(q.device, nbytes, ((B * spec.num_kv_heads * 4 + 255) // 256) * 256)
+    elif workspace.numel() * workspace.element_size() < nbytes:
+        raise ValueError(f"decode_step: workspace needs {nbytes} bytes")
+    st = lib.kvq_decode_step(
+        k.data_ptr(), v.data_ptr(), k.stride(0), v.stride(0), slot_mapping.data_ptr(), k.shape[0],
+        q.data_ptr(), q.stride(0), cache.pool.data_ptr(), cache.num_blocks, block_table.data_ptr(), max_blocks,
+        seq_lens.data_ptr(), B, Hq, spec.num_kv_heads, spec.kv_dtype_id, float(sm_scale), int(pps),
+        workspace.data_ptr(), workspace.numel() * workspace.element_size(), out.data_ptr(),
+        _lib.KVQ_OUT_F32 if out_dtype == torch.float32 else _lib.KVQ_OUT_BF16,
+        _lib.KVQ_OUT_HBD if head_major else _lib.KVQ_OUT_BHD, desc, _stream_handle(q.device))
+    _lib.check("kvq_decode_step", st)
+    return out
 
 
 def copy_blocks(cache: PagedKVCache, pairs: Sequence[Tuple[int, int]]) -> None:

@@ -26,7 +26,8 @@ import torch
 
 from . import _lib
 from .cache import PagedKVCache
-from .ops import paged_decode_attention, paged_decode_attention_gathered, quantize_append, workspace_bytes
+from .ops import (decode_step, paged_decode_attention, paged_decode_attention_gathered, quantize_append,
+                  workspace_bytes)
 
 
 class DecodeSession:
@@ -121,10 +122,19 @@ class DecodeSession:
                                pages_per_split=self.pps, out_dtype=self.out_dtype,
                                workspace=buf["ws"])
 
+    def step(self, buf) -> None:
+        """K1 + K2 of one step in one call (``kvq_decode_step``: K2's launch and
+        prologue overlap K1 through programmatic dependent launch)."""
+        decode_step(self.cache, buf["k"], buf["v"], buf["slots"], buf["q"], self.block_table, buf["lens"],
+                    sm_scale=self.sm_scale, pages_per_split=self.pps, out=buf["out"],
+                    out_dtype=self.out_dtype, head_major=self.head_major, workspace=buf["ws"],
+                    peer=self.peer, slot=buf["idx"])
+
     def _kernels(self, buf, k1: bool = True) -> None:
         if k1:
-            self.k1(buf)
-        self.k2(buf)
+            self.step(buf)
+        else:
+            self.k2(buf)
 
     def submit(self, q_h: torch.Tensor, k_h: torch.Tensor, v_h: torch.Tensor, slots_h: torch.Tensor,
                lens_h: torch.Tensor, out_h: torch.Tensor) -> torch.cuda.Event:
@@ -135,6 +145,8 @@ class DecodeSession:
     def _submit(self, inputs, out_h: torch.Tensor) -> torch.cuda.Event:
         buf = self.bufs[self.step_idx % self.depth]
         self.step_idx += 1
+        if inputs is None and buf.get("graph") is not None and out_h.is_pinned() and out_h.is_contiguous():
+            return self._submit_native(buf, out_h)
         with torch.cuda.stream(self.h2d):
             if buf["used"]:
                 self.h2d.wait_event(buf["done"])      # previous kernels finished reading
@@ -154,6 +166,31 @@ class DecodeSession:
             self.d2h.wait_event(buf["done"])
             out_h.copy_(full, non_blocking=True)
             buf["out_done"].record(self.d2h)
+        buf["used"] = True
+        return buf["out_done"]
+
+    def _submit_native(self, buf, out_h: torch.Tensor) -> torch.cuda.Event:
+        """A staged step whose slot graph exists: upload, graph launch and
+        download are enqueued by one native call (``kvq_pipeline_submit``)."""
+        import ctypes
+        full = buf["graph_out"]
+        nbytes = full.numel() * full.element_size()
+        if out_h.numel() * out_h.element_size() != nbytes:
+            raise ValueError(f"submit: out_h must hold {nbytes} bytes")
+        st = buf.get("pipe")
+        if st is None:
+            st = _lib.PipeStep()
+            st.h2d_stream, st.compute_stream = self.h2d.cuda_stream, self.compute.cuda_stream
+            st.d2h_stream = self.d2h.cuda_stream
+            st.graph_exec = buf["graph"].raw_cuda_graph_exec()
+            st.dev_in, st.host_in, st.in_bytes = buf["dev_in"].data_ptr(), buf["host_in"].data_ptr(), self.in_bytes
+            st.dev_out, st.out_bytes = full.data_ptr(), nbytes
+            st.ev_in_ready, st.ev_done = buf["in_ready"].cuda_event, buf["done"].cuda_event
+            st.ev_out_done = buf["out_done"].cuda_event
+            buf["pipe"] = st
+        st.host_out = out_h.data_ptr()
+        st.reuse = 1 if buf["used"] else 0
+        _lib.check("kvq_pipeline_submit", _lib.load().kvq_pipeline_submit(ctypes.byref(st)))
         buf["used"] = True
         return buf["out_done"]
 

@@ -7,7 +7,8 @@ import torch
 
 import oracle as O
 from kvq_testutil import Scenario
-from paper_2605_29639_b200 import KVCacheSpec, PagedKVCache, paged_decode_attention, quantize_append
+from paper_2605_29639_b200 import (KVCacheSpec, PagedKVCache, decode_step, paged_decode_attention,
+                                   quantize_append)
 from paper_2605_29639_b200.session import DecodeSession
 
 pytestmark = pytest.mark.gpu
@@ -124,3 +125,84 @@ def test_session_graphs_and_staged_match_eager(cuda, staged):
         assert torch.equal(a, b)
     assert torch.equal(caches[0].pool, caches[1].pool)
     assert len({int(o[0].float().sum()) for o in outs}) > 1, "inputs must change between steps"
+
+
+@pytest.mark.parametrize("kv_dtype", ["int8", "fp8_e4m3"])
+def test_decode_step_matches_two_calls(cuda, kv_dtype):
+    """kvq_decode_step (K2 PDL-launched behind K1) == quantize_append then
+    paged_decode_attention: identical pages, identical output, eager and in a
+    CUDA graph replayed with new rows; the appended rows are visible to K2."""
+    kvo = O.INT8 if kv_dtype == "int8" else O.FP8_E4M3
+    sc = Scenario([300, 17, 1020, 60, 1999], 32, 8, kvo, seed=21)  # each last page has room
+    pool0 = torch.from_numpy(sc.pool).to(cuda)
+    a = PagedKVCache(KVCacheSpec(8, kv_dtype=kv_dtype), sc.num_blocks, device=cuda, pool=pool0.clone())
+    b = PagedKVCache(KVCacheSpec(8, kv_dtype=kv_dtype), sc.num_blocks, device=cuda, pool=pool0.clone())
+    table = torch.from_numpy(sc.block_table).to(cuda)
+    # one new token per sequence at position seq_len (tables have room: extra blocks appended)
+    lens = sc.seq_lens.astype(np.int64)
+    assert all(lens[i] // 16 < -(-lens[i] // 16) for i in range(sc.B))
+    slots = torch.from_numpy((sc.block_table[np.arange(sc.B), lens // 16].astype(np.int64) * 16
+                              + lens % 16).astype(np.int32)).to(cuda)
+    lens1 = torch.from_numpy((lens + 1).astype(np.int32)).to(cuda)
+    g = torch.Generator(device=cuda).manual_seed(5)
+    k = torch.randn((sc.B, 8, 128), device=cuda, generator=g).to(torch.bfloat16)
+    v = torch.randn((sc.B, 8, 128), device=cuda, generator=g).to(torch.bfloat16)
+    q = torch.randn((sc.B, 32, 128), device=cuda, generator=g).to(torch.bfloat16)
+    out_a = decode_step(a, k, v, slots, q, table, lens1, out_dtype=torch.float32, pages_per_split=8)
+    quantize_append(b, k, v, slots)
+    out_b = paged_decode_attention(q, b, table, lens1, out_dtype=torch.float32, pages_per_split=8)
+    torch.cuda.synchronize()
+    assert torch.equal(a.pool, b.pool)
+    assert torch.equal(out_a, out_b)
+    # graph of the fused step, replayed with fresh rows
+    ws = torch.zeros(1 << 22, dtype=torch.uint8, device=cuda)
+    out_g = torch.empty((sc.B, 32, 128), dtype=torch.float32, device=cuda)
+    gr = torch.cuda.CUDAGraph()
+    decode_step(a, k, v, slots, q, table, lens1, out=out_g, out_dtype=torch.float32, pages_per_split=8,
+                workspace=ws)
+    torch.cuda.synchronize()
+    with torch.cuda.graph(gr):
+        decode_step(a, k, v, slots, q, table, lens1, out=out_g, out_dtype=torch.float32, pages_per_split=8,
+                    workspace=ws)
+    for _ in range(3):
+        k.copy_(torch.randn((sc.B, 8, 128), device=cuda, generator=g).to(torch.bfloat16))
+        v.copy_(torch.randn((sc.B, 8, 128), device=cuda, generator=g).to(torch.bfloat16))
+        gr.replay()
+        quantize_append(b, k, v, slots)
+        ref = paged_decode_attention(q, b, table, lens1, out_dtype=torch.float32, pages_per_split=8)
+        torch.cuda.synchronize()
+        assert torch.equal(a.pool, b.pool)
+        assert torch.equal(out_g, ref)
+
+
+def test_native_pipeline_back_to_back(cuda):
+    """submit_staged through the native submitter (kvq_pipeline_submit) with no
+    host synchronisation between steps: every step's download equals the
+    direct op calls for that step's inputs (slot reuse is event-ordered)."""
+    sc = Scenario([300, 40, 1200, 17, 64, 900], 32, 8, O.INT8, seed=31)
+    table = torch.from_numpy(sc.block_table).to(cuda)
+    pool0 = torch.from_numpy(sc.pool).to(cuda)
+    ref_cache = PagedKVCache(KVCacheSpec(8), sc.num_blocks, device=cuda, pool=pool0.clone())
+    sess = DecodeSession(PagedKVCache(KVCacheSpec(8), sc.num_blocks, device=cuda, pool=pool0.clone()),
+                         table, sc.B, 32, graphs=True)
+    g = torch.Generator().manual_seed(3)
+    lens = torch.from_numpy(sc.seq_lens)
+    slots = torch.tensor([int(sc.block_table[b, (L - 1) // 16]) * 16 + (L - 1) % 16
+                          for b, L in enumerate(sc.seq_lens)], dtype=torch.int32)
+    steps, refs, outs = 12, [], []
+    for step in range(steps):
+        q = torch.randn((sc.B, 32, 128), generator=g).to(torch.bfloat16)
+        k = torch.randn((sc.B, 8, 128), generator=g).to(torch.bfloat16)
+        v = torch.randn((sc.B, 8, 128), generator=g).to(torch.bfloat16)
+        quantize_append(ref_cache, k.to(cuda), v.to(cuda), slots.to(cuda))
+        refs.append(paged_decode_attention(q.to(cuda), ref_cache, table, lens.to(cuda)).cpu())
+        h = sess.next_inputs()                  # waits only for this slot's previous upload
+        for name, t in (("q", q), ("k", k), ("v", v), ("slots", slots), ("lens", lens)):
+            h[name].copy_(t)
+        o = torch.empty((sc.B, 32, 128), dtype=torch.bfloat16, pin_memory=True)
+        sess.submit_staged(o)
+        outs.append(o)
+    sess.synchronize()
+    assert all("pipe" in b for b in sess.bufs), "native submitter not used"
+    for a, b in zip(refs, outs):
+        assert torch.equal(a, b)

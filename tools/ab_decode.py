@@ -14,7 +14,7 @@ import sys
 import numpy as np
 import torch
 
-SHAPES = {"c2": (256, 32, 8, "ragged", 0), "c3": (128, 64, 8, 32768, 1), "c4": (64, 64, 4, 131072, 0)}
+SHAPES = {"c1": (8, 32, 8, 2048, 0), "c2": (256, 32, 8, "ragged", 0), "c3": (128, 64, 8, 32768, 1), "c4": (64, 64, 4, 131072, 0)}
 
 
 def main():

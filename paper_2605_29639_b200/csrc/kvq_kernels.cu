@@ -58,67 +58,95 @@ __host__ __device__ __forceinline__ int v_code_off(int tok, int d) {
 // ---------------------------------------------------------------------------
 // K1: quantize-on-append.  CTA = 16 consecutive tokens x 4 kv heads; an
 // 8-lane group owns one (token pair 2p/2p+1, head): its 4 rows (K and V of
-// both tokens, 16 elements per lane) are loaded up front with LDG.128, reduced
-// over 8 lanes, and written
-//   * as a whole page image in shared memory, then 16-byte coalesced stores,
-//     when the 16 tokens fill one page (slots blk*16 + 0..15: chunked prefill);
-//   * directly otherwise (decode: one token per sequence), V as interleaved
+// both tokens, 16 elements per lane) are loaded up front with LDG.128 and
+// their amax reduced over the 8 lanes.  Each lane then performs ONE of the
+// group's 8 IEEE divisions (the scale or the inverse of one row) and the
+// results are shuffled to where they are needed.  INT8 codes come from the
+// exact round-to-nearest-even of an fp32 add of 1.5 * 2^23 (|y| <= 127 lands
+// in the low mantissa byte) and byte permutes; rows holding NaN / inf, or
+// whose inverse overflows (subnormal amax), take the F2I path instead, so the
+// contract of DESIGN.md §3 holds bit for bit.  Output:
+//   * whole page (slots blk*16 + 0..15: chunked prefill): the page image is
+//     built in shared memory (st.shared, base + immediate offsets) and
+//     written by one TMA bulk store per (block, head);
+//   * otherwise (scattered tokens): direct global stores, V as interleaved
 //     16-byte chunks when the pair's two slots are adjacent, else byte-wise.
 // ---------------------------------------------------------------------------
 constexpr int K1_THREADS = 256;
 constexpr int K1_HEADS = 4;
 
-// Quantize 16 values held by this lane of an 8-lane row group (contract).
-template <int KVD>
-__device__ __forceinline__ void quantize16(const uint4 lo, const uint4 hi, float& scale_out,
-                                           uint32_t (&codes)[4]) {
-  float x[16];
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ float max_nan(float a, float b) {
+  float d;
+  asm("max.NaN.f32 %0, %1, %2;" : "=f"(d) : "f"(a), "f"(b));
+  return d;
+}
+__device__ __forceinline__ void bf16x16(const uint4 lo, const uint4 hi, float (&x)[16]) {
   const uint32_t w[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
     x[2 * i] = __uint_as_float(w[i] << 16);
     x[2 * i + 1] = __uint_as_float(w[i] & 0xffff0000u);
   }
-  float a = 0.0f;
-#pragma unroll
-  for (int i = 0; i < 16; ++i) a = fmaxf(a, fabsf(x[i]));
-#pragma unroll
-  for (int o = 1; o < 8; o <<= 1) a = fmaxf(a, __shfl_xor_sync(FULL, a, o));
-  const float qmax = KVD == KVQ_FP8_E4M3 ? 448.0f : 127.0f;
-  scale_out = __fdiv_rn(a, qmax);
-  const float inv = a > 0.0f ? __fdiv_rn(qmax, a) : 0.0f;
+}
+// INT8 codes of 16 values (contract).  FAST: no NaN / inf in
+// the row and a finite inverse, so y = x * inv is finite with |y| <= 127 (1 + 2^-24):
+// y + 1.5 * 2^23 rounds to the integer rint_even(y) (ulp 1, RN-even), which the
+// clamp to +-127 cannot change, and its low byte is the code.
+template <bool FAST>
+__device__ __forceinline__ void int8x16(const float (&x)[16], float inv, uint32_t (&codes)[4]) {
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
-    float y[4];
+    if constexpr (FAST) {
+      uint32_t r[4];
 #pragma unroll
-    for (int e = 0; e < 4; ++e) y[e] = __fmul_rn(x[4 * i + e], inv);
-    if constexpr (KVD == KVQ_FP8_E4M3) {
-      uint16_t l, h;
-      asm("cvt.rn.satfinite.e4m3x2.f32 %0, %1, %2;" : "=h"(l) : "f"(y[1]), "f"(y[0]));
-      asm("cvt.rn.satfinite.e4m3x2.f32 %0, %1, %2;" : "=h"(h) : "f"(y[3]), "f"(y[2]));
-      codes[i] = (uint32_t)l | ((uint32_t)h << 16);
+      for (int e = 0; e < 4; ++e) r[e] = __float_as_uint(__fadd_rn(__fmul_rn(x[4 * i + e], inv), 12582912.0f));
+      codes[i] = __byte_perm(__byte_perm(r[0], r[1], 0x0040), __byte_perm(r[2], r[3], 0x0040), 0x5410);
     } else {
       uint32_t word = 0;
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
-        const int c = max(-127, min(127, __float2int_rn(y[e])));  // NaN -> 0, saturating
+        const int c = max(-127, min(127, __float2int_rn(__fmul_rn(x[4 * i + e], inv))));  // NaN -> 0
         word |= ((uint32_t)(c & 0xff)) << (8 * e);
       }
       codes[i] = word;
     }
   }
 }
+__device__ __forceinline__ void e4m3x16(const float (&x)[16], float inv, uint32_t (&codes)[4]) {
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    float y[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) y[e] = __fmul_rn(x[4 * i + e], inv);
+    uint16_t l, h;
+    asm("cvt.rn.satfinite.e4m3x2.f32 %0, %1, %2;" : "=h"(l) : "f"(y[1]), "f"(y[0]));
+    asm("cvt.rn.satfinite.e4m3x2.f32 %0, %1, %2;" : "=h"(h) : "f"(y[3]), "f"(y[2]));
+    codes[i] = (uint32_t)l | ((uint32_t)h << 16);
+  }
+}
+__device__ __forceinline__ void sts32(uint32_t a, uint32_t v) {
+  asm volatile("st.shared.b32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+__device__ __forceinline__ void sts128(uint32_t a, uint4 v) {
+  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+               : "memory");
+}
 
 template <int KVD>
-__global__ void __launch_bounds__(K1_THREADS) quant_append_kernel(
+__global__ void __launch_bounds__(K1_THREADS, 3) quant_append_kernel(  // 80 regs, no spills
     const __nv_bfloat16* __restrict__ k, const __nv_bfloat16* __restrict__ v, int64_t k_stride,
     int64_t v_stride, const int32_t* __restrict__ slots, int T, int Hkv,
     uint8_t* __restrict__ pool, int64_t num_blocks) {
   // A K2 launched behind this kernel with programmatic serialization may start
   // its prologue now; it waits (griddepcontrol.wait) before reading any page.
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-  __shared__ __align__(16) uint8_t img[K1_HEADS][PAGE];
+  __shared__ __align__(128) uint8_t img[K1_HEADS][PAGE];
   const int t0 = blockIdx.x * 16, h0 = blockIdx.y * K1_HEADS;
+  const int lane = threadIdx.x & 31;
   const int grp = threadIdx.x >> 3, j = threadIdx.x & 7;  // lane j of the group owns d [16j, 16j+16)
   const int hh = grp >> 3, pp = grp & 7;                  // head h0+hh, tokens t0+2pp, t0+2pp+1
   const int h = h0 + hh;
@@ -136,7 +164,6 @@ __global__ void __launch_bounds__(K1_THREADS) quant_append_kernel(
     }
   }
   int slot[2];
-  bool live[2];
 #pragma unroll
   for (int i = 0; i < 2; ++i) {
     const int t = t0 + 2 * pp + i;
@@ -150,62 +177,137 @@ __global__ void __launch_bounds__(K1_THREADS) quant_append_kernel(
                        (my_slot >= 0 && my_slot == first + (int)threadIdx.x && (first & 15) == 0 &&
                         (first >> 4) < num_blocks);
   const bool whole = __syncthreads_and(mine_ok);
+
+  // ---- per-row amax over the 8 lanes (NaN-propagating for INT8: flags NaN rows)
+  const float qmax = KVD == KVQ_FP8_E4M3 ? 448.0f : 127.0f;
+  float am[4];  // row rr = 2 * token + kv
+#pragma unroll
+  for (int rr = 0; rr < 4; ++rr) {
+    float x[16];
+    bf16x16(raw[rr >> 1][rr & 1][0], raw[rr >> 1][rr & 1][1], x);
+    float a = 0.0f;
+#pragma unroll
+    for (int e = 0; e < 16; ++e) a = KVD == KVQ_INT8 ? max_nan(a, fabsf(x[e])) : fmaxf(a, fabsf(x[e]));
+#pragma unroll
+    for (int o = 1; o < 8; o <<= 1) {
+      const float b = __shfl_xor_sync(FULL, a, o);
+      a = KVD == KVQ_INT8 ? max_nan(a, b) : fmaxf(a, b);
+    }
+    am[rr] = a;
+  }
+  bool nanrow[4] = {false, false, false, false};
+  if (KVD == KVQ_INT8 && __any_sync(FULL, am[0] != am[0] || am[1] != am[1] || am[2] != am[2] || am[3] != am[3])) {
+#pragma unroll
+    for (int rr = 0; rr < 4; ++rr) {  // rare: NaN-ignoring amax of the rows that hold NaN
+      nanrow[rr] = am[rr] != am[rr];
+      float x[16];
+      bf16x16(raw[rr >> 1][rr & 1][0], raw[rr >> 1][rr & 1][1], x);
+      float a = 0.0f;
+#pragma unroll
+      for (int e = 0; e < 16; ++e) a = fmaxf(a, fabsf(x[e]));
+#pragma unroll
+      for (int o = 1; o < 8; o <<= 1) a = fmaxf(a, __shfl_xor_sync(FULL, a, o));
+      if (nanrow[rr]) am[rr] = a;
+    }
+  }
+  // ---- one IEEE division per lane: lane j -> row j & 3, scale (j >= 4) or inverse (j < 4)
+  float dv;
+  {
+    const int rr = j & 3;
+    const float a = rr == 0 ? am[0] : rr == 1 ? am[1] : rr == 2 ? am[2] : am[3];
+    const bool is_scale = j >= 4;
+    dv = __fdiv_rn(is_scale ? a : qmax, is_scale ? qmax : a);
+    if (!is_scale && !(a > 0.0f)) dv = 0.0f;
+  }
+  float inv[4];
+#pragma unroll
+  for (int rr = 0; rr < 4; ++rr) inv[rr] = __shfl_sync(FULL, dv, (lane & ~7) | rr);
+
+  // ---- codes: [token][K|V][4 words]
+  uint32_t code[2][2][4];
+#pragma unroll
+  for (int rr = 0; rr < 4; ++rr) {
+    float x[16];
+    bf16x16(raw[rr >> 1][rr & 1][0], raw[rr >> 1][rr & 1][1], x);
+    if constexpr (KVD == KVQ_FP8_E4M3) {
+      e4m3x16(x, inv[rr], code[rr >> 1][rr & 1]);
+    } else {
+      const bool fast = !nanrow[rr] && am[rr] < INFINITY && inv[rr] < INFINITY;  // uniform per group
+      if (fast) int8x16<true>(x, inv[rr], code[rr >> 1][rr & 1]);
+      else int8x16<false>(x, inv[rr], code[rr >> 1][rr & 1]);
+    }
+  }
+  // V codes of the token pair interleaved: bytes (d, t0), (d, t1) for d = 16j .. 16j+15
+  // form logical pair-row bytes [32j, 32j+32) = two 16-byte chunks.
+  uint32_t il[8];
+#pragma unroll
+  for (int w = 0; w < 4; ++w) {
+    il[2 * w] = __byte_perm(code[0][1][w], code[1][1][w], 0x5140);
+    il[2 * w + 1] = __byte_perm(code[0][1][w], code[1][1][w], 0x7362);
+  }
+  const int rs = j & 3, ts = rs >> 1;  // the scale this lane holds (j >= 4): row rs, token ts
+
+  if (whole) {
+    // ---- page image in shared memory; K word w of token tok sits at
+    //      p*256 + 16c + (2*half + hi)*4 + 64*(w ^ (p & 1)), p = tok & 7 (p & 1 == i here)
+    const uint32_t img_s = smem_u32(img[hh]);
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      const int tok = 2 * pp + i, p = tok & 7;
+      const uint32_t kb = img_s + p * 256 + 16 * (j & 3) + (2 * (j >> 2) + (tok >> 3)) * 4;
+#pragma unroll
+      for (int w = 0; w < 4; ++w) sts32(kb + 64 * (w ^ i), code[i][0][w]);
+    }
+#pragma unroll
+    for (int half = 0; half < 2; ++half)
+      sts128(img_s + v_code_off(2 * pp, 16 * j + 8 * half),
+             make_uint4(il[4 * half], il[4 * half + 1], il[4 * half + 2], il[4 * half + 3]));
+    if (j >= 4) sts32(img_s + ((rs & 1) ? VS_OFF : KS_OFF) + 4 * (2 * pp + ts), __float_as_uint(dv));
+    // generic-proxy smem writes -> visible to the bulk copy (async proxy)
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncthreads();
+    const int nh = min(K1_HEADS, Hkv - h0);
+    if (threadIdx.x < nh) {
+      uint8_t* dst = pool + ((int64_t)(first >> 4) * Hkv + h0 + threadIdx.x) * PAGE;
+      asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst),
+                   "r"(smem_u32(img[threadIdx.x])), "n"(PAGE)
+                   : "memory");
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    }
+    return;
+  }
+
+  // ---- scattered tokens: direct global stores
+  bool live[2];
 #pragma unroll
   for (int i = 0; i < 2; ++i) live[i] = slot[i] >= 0 && (slot[i] >> 4) < num_blocks && h < Hkv;
-  uint32_t code[2][2][4];
-  float scale[2][2];
-#pragma unroll
-  for (int i = 0; i < 2; ++i)
-#pragma unroll
-    for (int kv = 0; kv < 2; ++kv) quantize16<KVD>(raw[i][kv][0], raw[i][kv][1], scale[i][kv], code[i][kv]);
-
   const bool pair_adj = live[0] && live[1] && (slot[0] & 1) == 0 && slot[1] == slot[0] + 1;
 #pragma unroll
   for (int i = 0; i < 2; ++i) {
     if (!live[i]) continue;
     const int tok = slot[i] & 15;
-    uint8_t* page = whole ? img[hh] : pool + ((int64_t)(slot[i] >> 4) * Hkv + h) * PAGE;
+    uint8_t* page = pool + ((int64_t)(slot[i] >> 4) * Hkv + h) * PAGE;
 #pragma unroll
     for (int w = 0; w < 4; ++w)
       *reinterpret_cast<uint32_t*>(page + k_code_off(tok, 16 * j + 4 * w)) = code[i][0][w];
-    if (!(whole || pair_adj)) {  // lone token: V bytes at 2d + (tok & 1)
+    if (!pair_adj) {  // lone token: V bytes at 2d + (tok & 1)
 #pragma unroll
       for (int w = 0; w < 4; ++w)
 #pragma unroll
         for (int e = 0; e < 4; ++e)
           page[v_code_off(tok, 16 * j + 4 * w + e)] = (uint8_t)(code[i][1][w] >> (8 * e));
     }
-    if (j == 0) {
-      *reinterpret_cast<float*>(page + KS_OFF + 4 * tok) = scale[i][0];
-      *reinterpret_cast<float*>(page + VS_OFF + 4 * tok) = scale[i][1];
-    }
+    if (j >= 4 && ts == i)
+      *reinterpret_cast<float*>(page + ((rs & 1) ? VS_OFF : KS_OFF) + 4 * tok) = dv;
   }
-  if (whole || pair_adj) {
-    // Interleave the pair's V codes: bytes (d, t0), (d, t1) for d = 16j .. 16j+15 form the
-    // logical pair-row range [32j, 32j+32) = two 16-byte chunks.
-    uint32_t il[8];
-#pragma unroll
-    for (int w = 0; w < 4; ++w) {
-      il[2 * w] = __byte_perm(code[0][1][w], code[1][1][w], 0x5140);
-      il[2 * w + 1] = __byte_perm(code[0][1][w], code[1][1][w], 0x7362);
-    }
+  if (pair_adj) {
     const int tok = slot[0] & 15;  // even
-    uint8_t* page = whole ? img[hh] : pool + ((int64_t)(slot[0] >> 4) * Hkv + h) * PAGE;
+    uint8_t* page = pool + ((int64_t)(slot[0] >> 4) * Hkv + h) * PAGE;
 #pragma unroll
-    for (int half = 0; half < 2; ++half) {
-      const int dd = 16 * j + 8 * half;  // d of the chunk's first byte pair
-      *reinterpret_cast<uint4*>(page + v_code_off(tok, dd)) =
+    for (int half = 0; half < 2; ++half)
+      *reinterpret_cast<uint4*>(page + v_code_off(tok, 16 * j + 8 * half)) =
           make_uint4(il[4 * half], il[4 * half + 1], il[4 * half + 2], il[4 * half + 3]);
-    }
-  }
-  if (whole) {
-    __syncthreads();
-    const int nh = min(K1_HEADS, Hkv - h0);
-    for (int x = 0; x < nh; ++x) {
-      uint4* dst = reinterpret_cast<uint4*>(pool + ((int64_t)(first >> 4) * Hkv + h0 + x) * PAGE);
-      const uint4* src = reinterpret_cast<const uint4*>(img[x]);
-      for (int i = threadIdx.x; i < PAGE / 16; i += K1_THREADS) dst[i] = src[i];
-    }
   }
 }
 
@@ -287,9 +389,6 @@ __global__ void __launch_bounds__(K1R_WARPS * 32) quant_append_rows_kernel(
 // ---------------------------------------------------------------------------
 // PTX helpers: shared-memory addresses, mbarriers, bulk async copy, MMA.
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
 }
@@ -443,8 +542,14 @@ constexpr int THREADS = 32 * NW;
 template <bool HI>
 struct Geo {
   static constexpr int NT = HI ? 2 : 1;
-  static constexpr int S = 3;                     // ring slots (pages in flight) per warp
-  static constexpr int CTAS = 4;                  // resident CTAs per SM (regs + smem)
+#ifndef KVQ_HI_S
+#define KVQ_HI_S 3
+#endif
+#ifndef KVQ_HI_CTAS
+#define KVQ_HI_CTAS 4
+#endif
+  static constexpr int S = HI ? KVQ_HI_S : 3;          // ring slots (pages in flight) per warp
+  static constexpr int CTAS = HI ? KVQ_HI_CTAS : 4;    // resident CTAs per SM (regs + smem)
   // g > 8 keeps the Q^T fragments in shared memory (one copy per CTA, read with
   // one conflict-free LDS.64 per k-step) so the live set fits 128 registers.
   static constexpr size_t QSM = HI ? (size_t)NT * 8 * 32 * 8 : 0;  // [nt][k-step pair][lane] uint4

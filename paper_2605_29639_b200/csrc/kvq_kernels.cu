@@ -1,15 +1,18 @@
 // kvq_kernels.cu -- sm_100a kernels for the quantized paged-KV decode path and
 // the C ABI declared in include/kvq.h.
 //
-//   K1 quant_append_kernel   bf16 K/V rows -> per-(token, head) scale + 8-bit
-//                            codes scattered into the paged pool.
-//   K2 decode_kernel         warp-specialised paged GQA decode attention:
-//                            1 producer warp streams 4224-byte pages with
-//                            cp.async.bulk (TMA bulk copy) into an mbarrier
-//                            ring; 4 consumer warps dequantise in registers
-//                            and run QK^T / PV on the tensor cores
-//                            (mma.sync m16n8k16 f16 -> f32), online softmax,
-//                            fused split-KV combine by the last CTA.
+//   K1 quant_append_kernel /   bf16 K/V rows -> per-(token, head) scale + 8-bit
+//      quant_append_rows_kernel   codes in the paged pool (whole pages via a
+//                            shared-memory image + TMA bulk store; scattered
+//                            decode rows one warp per (token, head)).
+//   K2 decode_kernel         paged GQA decode attention: every warp streams its
+//                            own 4224-byte pages with cp.async.bulk (TMA bulk
+//                            copy) into a 3-slot mbarrier ring, QK^T on the s8
+//                            (INT8 K) or f16 (E4M3 K) tensor cores, online
+//                            softmax with lazy rescale, PV on f16 tensor cores,
+//                            fused split-KV combine by the last CTA; variants
+//                            for multi-query scoring and for the KV-head output
+//                            gather fused over peer memory.
 //   K3 copy_blocks_kernel    page copies for copy-on-write of shared tails.
 //
 // Layouts and the rounding contract: DESIGN.md §2-§3.  The CPU restatement

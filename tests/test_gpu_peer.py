@@ -1,11 +1,11 @@
 """The all-gather fused into K2 (kvq_decode_attn_peer), end to end on one GPU.
 
-Two processes play two ranks on cuda:0 and map each other's symmetric
+Two (or four) processes play the ranks on cuda:0 and map each other's symmetric
 buffers through CUDA IPC -- the same peer pointers, stores, release/acquire
 flags and slot protocol that NVLink peers use across GPUs; only the wire
 differs.  Each rank attends its shard (KV-head split, or the 2-D split's batch
-part with the LPT seq_map) and its K2 writes every finished row into both
-ranks' global outputs.  Checked, for several uses of two slots, eager and
+part with the LPT seq_map) and its K2 writes every finished row into every
+rank's global output.  Checked, for several uses of two slots, eager and
 CUDA-graph replays and the DecodeSession pipeline: every rank's global output
 equals the unsharded kernel's output bit for bit (same split geometry), and no
 protocol spin timed out."""
@@ -48,8 +48,10 @@ def _worker(rank, world, port, mode, result_q):
         torch.cuda.set_device(dev)
         if mode == "head":      # KV-head tensor parallelism (Hkv % P == 0)
             Hq, Hkv, lens = 32, 8, [70, 33, 150, 0, 400, 17]
-        else:                   # 2-D: one KV head, batch halves balanced by LPT (seq_map)
+        elif mode == "batch":   # one KV head, batch halves balanced by LPT (seq_map)
             Hq, Hkv, lens = 8, 1, [70, 33, 150, 0, 400, 17, 260]
+        else:                   # 2-D at world 4: 2 KV-head groups x 2 LPT batch parts (the C4-at-8 shape)
+            Hq, Hkv, lens = 16, 2, [70, 33, 150, 0, 400, 17, 260, 90]
         sc = Scenario(lens, Hq, Hkv, O.INT8, seed=9)          # identical bytes on every rank
         B = sc.B
         pps = 4
@@ -121,9 +123,8 @@ def _worker(rank, world, port, mode, result_q):
     result_q.put((rank, checks))
 
 
-@pytest.mark.parametrize("mode", ["head", "batch"])
-def test_fused_peer_gather_two_ranks_one_gpu(cuda, mode):
-    world = 2
+@pytest.mark.parametrize("mode,world", [("head", 2), ("batch", 2), ("2d", 4)])
+def test_fused_peer_gather_ranks_on_one_gpu(cuda, mode, world):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()

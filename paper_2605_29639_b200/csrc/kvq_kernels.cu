@@ -276,7 +276,9 @@ __global__ void __launch_bounds__(K1_THREADS, 3) quant_append_kernel(  // 80 reg
                    "r"(smem_u32(img[threadIdx.x])), "n"(PAGE)
                    : "memory");
       asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-      asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+      // Only the shared-memory reads must finish before the CTA exits (and its
+      // smem is reused); the global writes complete with the grid.
+      asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
     }
     return;
   }
@@ -1396,8 +1398,10 @@ int kvq_quant_append(const void* k, const void* v, int64_t k_token_stride, int64
   const auto kp = static_cast<const __nv_bfloat16*>(k);
   const auto vp = static_cast<const __nv_bfloat16*>(v);
   auto* pp = static_cast<uint8_t*>(pool);
-  if ((int64_t)T * Hkv <= kvq::K1_ROWS_MAX) {
-    // Decode-shaped batch: latency-bound, one warp per (token, head).
+  const bool rows16 = aligned(k, 16) && aligned(v, 16) && (k_token_stride % 8) == 0 && (v_token_stride % 8) == 0;
+  if ((int64_t)T * Hkv <= kvq::K1_ROWS_MAX || !rows16) {
+    // Decode-shaped batch (latency-bound), or rows only 8-byte aligned (the tile
+    // kernels load 16 bytes per lane): one warp per (token, head).
     const unsigned nblk = (unsigned)((T * Hkv + kvq::K1R_WARPS - 1) / kvq::K1R_WARPS);
     if (kv_dtype == KVQ_INT8)
       kvq::quant_append_rows_kernel<KVQ_INT8><<<nblk, kvq::K1R_WARPS * 32, 0, st>>>(
@@ -1407,7 +1411,8 @@ int kvq_quant_append(const void* k, const void* v, int64_t k_token_stride, int64
           kp, vp, k_token_stride, v_token_stride, slot_mapping, T, Hkv, pp, num_blocks);
     return check_launch("quant_append");
   }
-  const dim3 grid((unsigned)((T + 15) / 16), (unsigned)((Hkv + kvq::K1_HEADS - 1) / kvq::K1_HEADS));
+  const int HG = (Hkv + kvq::K1_HEADS - 1) / kvq::K1_HEADS;
+  const dim3 grid((unsigned)((T + 15) / 16), (unsigned)HG);
   if (kv_dtype == KVQ_INT8)
     kvq::quant_append_kernel<KVQ_INT8><<<grid, kvq::K1_THREADS, 0, st>>>(
         kp, vp, k_token_stride, v_token_stride, slot_mapping, T, Hkv, pp, num_blocks);

@@ -117,3 +117,46 @@ def test_append_whole_pages_and_mixed(cuda, kv_dtype, tile):
     k, v = make_kv(T, Hkv, 31, kind="k"), make_kv(T, Hkv, 32, kind="v")
     gpu, ref = run_both(k, v, slots, Hkv, kv_dtype, num_blocks, cuda, tile=tile)
     assert np.array_equal(gpu, ref), f"{(gpu != ref).sum()} bytes differ"
+
+
+@pytest.mark.parametrize("kv_dtype", ["int8", "fp8_e4m3"])
+@pytest.mark.parametrize("aligned16", [True, False])
+def test_large_append_alignments(cuda, kv_dtype, aligned16):
+    """Large appends take the 16-token tile kernel when K/V rows are 16-byte
+    aligned, else the one-warp-per-row kernel (the tile kernel loads 16 bytes
+    per lane): bit-exact either way, with a partial head group (Hkv = 6), a
+    partial last tile, whole-page tiles mixed with scattered and skipped
+    tokens, and strided K/V slices of a fused buffer."""
+    Hkv, nb = 6, 900
+    rng = np.random.default_rng(17)
+    perm = rng.permutation(nb)
+    slots, used = [], 0
+    for p in range(600):                 # whole pages (chunked prefill)
+        slots += [int(perm[used]) * 16 + t for t in range(16)]
+        used += 1
+    for _ in range(150):                 # scattered decode tokens, some pairs adjacent
+        blk = int(perm[used]); used += 1
+        o = int(rng.integers(0, 15))
+        slots += [blk * 16 + o, blk * 16 + o + 1] if rng.random() < 0.5 else [blk * 16 + o]
+    slots += [-1] * 5 + [int(perm[used]) * 16 + 3]
+    slots += [int(perm[used + 1]) * 16 + t for t in range(9)]   # partial last tile
+    T = len(slots)
+    assert T % 16 and T * Hkv > 8192
+    # fused [T, Hq + 2 Hkv, 128] buffer; one extra element shifts the rows off 16 B when not aligned16
+    width = 3 * Hkv * 128 + (0 if aligned16 else 4)
+    buf = torch.zeros((T, width), dtype=torch.bfloat16)
+    k = make_kv(T, Hkv, 41, kind="k")
+    v = make_kv(T, Hkv, 42, kind="v")
+    off = 0 if aligned16 else 4
+    buf[:, off + Hkv * 128: off + 2 * Hkv * 128] = k.reshape(T, -1)
+    buf[:, off + 2 * Hkv * 128: off + 3 * Hkv * 128] = v.reshape(T, -1)
+    bd = buf.to(cuda)
+    kd = bd[:, off + Hkv * 128: off + 2 * Hkv * 128].view(T, Hkv, 128)
+    vd = bd[:, off + 2 * Hkv * 128: off + 3 * Hkv * 128].view(T, Hkv, 128)
+    assert (kd.data_ptr() % 16 == 0) == aligned16
+    cache = PagedKVCache(KVCacheSpec(Hkv, kv_dtype=kv_dtype), nb, device=cuda)
+    quantize_append(cache, kd, vd, torch.as_tensor(slots, dtype=torch.int32, device=cuda))
+    ref = np.zeros((nb, Hkv, O.PAGE), dtype=np.uint8)
+    O.quant_append(bf16_bits(k), bf16_bits(v), np.asarray(slots, np.int32), DT[kv_dtype], ref)
+    gpu = cache.pool.cpu().numpy()
+    assert np.array_equal(gpu, ref), int((gpu != ref).sum())

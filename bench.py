@@ -213,7 +213,7 @@ def run_reference(args, cfg):
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3,
-        "higher_is_better": True, "scaling": "strong" if args.gpus > 1 else "weak",
+        "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": cfg["kv"].replace("fp8_e4m3", "e4m3"), "data": "synthetic",
         "config": {"workload": cfg["workload"], "sample": sample.describe()},
         "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": sample.threads, "kind": "port",
@@ -489,7 +489,7 @@ def run_ours(args, cfg):
     line = {
         "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
-        "scaling": "strong" if world > 1 else "weak", "vs_baseline": None,
+        "scaling": "strong", "vs_baseline": None,
         "dtype": cfg["kv"].replace("fp8_e4m3", "e4m3"), "data": "synthetic",
         "config": {"workload": cfg["workload"], "name": args.config, "global_batch": B,
                    "sum_ctx": int((lens_all + 1).sum()),
@@ -654,7 +654,7 @@ def run_c5(args, cfg):
     line = {
         "metric": METRIC, "value": B / (ms_step * 1e-3), "unit": "tokens/s", "n_gpus": 1,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": cfg["kv"].replace("fp8_e4m3", "e4m3"),
+        "scaling": "strong", "vs_baseline": None, "dtype": cfg["kv"].replace("fp8_e4m3", "e4m3"),
         "data": "synthetic",
         "config": {"workload": cfg["workload"], "name": "c5", "decode_seqs": B, "sum_ctx": int(ctx.sum()),
                    "prefill_tokens_per_step": len(pf_slots), "prefix_groups": ngroups,

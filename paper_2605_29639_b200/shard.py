@@ -265,14 +265,30 @@ class PeerOutput:
             handles: List[Optional[bytes]] = [None] * self.P
             dist.all_gather_object(handles, bytes(handle), group=group)
             self._bases, self._opened = [], []
+            err = None
             for r, h in enumerate(handles):
                 if r == self.rank:
                     self._bases.append(self._own)
                     continue
                 p = ctypes.c_void_p()
-                _lib.check("kvq_sym_open", lib.kvq_sym_open(h, ctypes.byref(p)))
+                st = lib.kvq_sym_open(h, ctypes.byref(p))
+                if st != _lib.KVQ_OK:
+                    err = f"rank {self.rank}: kvq_sym_open of rank {r}: {lib.kvq_last_error().decode()}"
+                    break
                 self._bases.append(p.value)
                 self._opened.append(p.value)
+            # Every rank must agree before anyone relies on the mapping: a rank
+            # that cannot map its peers makes all ranks raise (and fall back),
+            # instead of leaving the others waiting in a barrier.
+            errs: List[Optional[str]] = [None] * self.P
+            dist.all_gather_object(errs, err, group=group)
+            failed = [e for e in errs if e]
+            if failed:
+                for q in self._opened:
+                    lib.kvq_sym_close(q)
+                lib.kvq_sym_free(self._own)
+                self._own, self._opened = None, []
+                raise RuntimeError("fused peer gather unavailable: " + "; ".join(failed))
         self.group = group
         # rows of this rank's sequences in the global output (identity for a pure head split)
         self.seq_map = (None if plan.b_split == 1 else

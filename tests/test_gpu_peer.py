@@ -123,6 +123,46 @@ def _worker(rank, world, port, mode, result_q):
     result_q.put((rank, checks))
 
 
+def _fail_worker(rank, world, port, result_q):
+    """Rank 1 cannot map its peer: every rank must raise (no rank left in a barrier)."""
+    import sys
+    from pathlib import Path
+    sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+    import torch
+    import torch.distributed as dist
+    from paper_2605_29639_b200 import _lib
+    from paper_2605_29639_b200.shard import PeerOutput, plan_shards
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    torch.cuda.set_device(0)
+    if rank == 1:
+        lib = _lib.load()
+        lib.kvq_sym_open = lambda handle, ptr: _lib.KVQ_ECUDA   # simulated IPC failure
+    try:
+        PeerOutput(plan_shards(32, 8, world, rank, [100] * 4), 32, 4, 8, torch.device("cuda:0"))
+        result_q.put((rank, "no error"))
+    except RuntimeError as e:
+        result_q.put((rank, "raised" if "unavailable" in str(e) else str(e)))
+    dist.destroy_process_group()
+
+
+def test_peer_setup_failure_is_collective(cuda):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_fail_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    try:
+        res = dict(q.get(timeout=300) for _ in range(2))
+    finally:
+        for p in procs:
+            p.join(timeout=60)
+            if p.is_alive():
+                p.kill()
+    assert res == {0: "raised", 1: "raised"}
+
+
 @pytest.mark.parametrize("mode,world", [("head", 2), ("batch", 2), ("2d", 4)])
 def test_fused_peer_gather_ranks_on_one_gpu(cuda, mode, world):
     ctx = mp.get_context("spawn")

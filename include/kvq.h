@@ -121,6 +121,14 @@ int kvq_decode_attn_mq(const void* q, int64_t q_batch_stride, int32_t q_len, con
  * pairs[2*i+1] = dst block (device int32). */
 int kvq_copy_blocks(void* pool, int64_t num_blocks, int32_t Hkv, const int32_t* pairs,
                     int32_t n_pairs, void* stream);
+/* PD KV transfer (replaces the payload of _migrate_kv,
+ * simulator.py:485-497): gather blocks block_ids[0..n) of the pool (all kv
+ * heads) into a packed uint8 [n][Hkv][KVQ_PAGE_BYTES] buffer -- the wire
+ * format -- and scatter such a buffer into the receiver's blocks. */
+int kvq_gather_blocks(const void* pool, int64_t num_blocks, int32_t Hkv, const int32_t* block_ids,
+                      int32_t n, void* out, void* stream);
+int kvq_scatter_blocks(void* pool, int64_t num_blocks, int32_t Hkv, const int32_t* block_ids,
+                       int32_t n, const void* in, void* stream);
 
 /* ---- KV-head sharding with the output all-gather fused into K2 ----------
  * Replaces the separate all-gather of the sharded decode (the

@@ -37,6 +37,8 @@ SIGNATURES = {
     "kvq_decode_attn_mq": (_c.c_int, [_vp, _i64, _i32, _vp, _i64, _vp, _i32, _vp, _i32, _i32, _i32,
                                       _i32, _f32, _i32, _vp, _sz, _vp, _i32, _i32, _vp]),
     "kvq_copy_blocks": (_c.c_int, [_vp, _i64, _i32, _vp, _i32, _vp]),
+    "kvq_gather_blocks": (_c.c_int, [_vp, _i64, _i32, _vp, _i32, _vp, _vp]),
+    "kvq_scatter_blocks": (_c.c_int, [_vp, _i64, _i32, _vp, _i32, _vp, _vp]),
     "kvq_block_hashes": (_i64, [_vp, _i64, _i32, _c.c_uint64, _vp]),
     "kvq_decode_attn_peer": (_c.c_int, [_vp, _i64, _vp, _i64, _vp, _i32, _vp, _i32, _i32, _i32, _i32,
                                         _f32, _i32, _vp, _sz, _vp, _vp]),

@@ -11,9 +11,9 @@ pages are bit-identical to the prefill worker's.
 
 Transport is ``torch.distributed`` point-to-point: NCCL over NVLink between
 GPUs, or gloo in the CPU tests.  Pages are gathered into one contiguous
-staging buffer with a single ``index_select`` and scattered on arrival with a
-single ``index_copy_``.  Both are device-side copies, so the only
-host<->device traffic is the 16-byte header.
+staging buffer by one ``kvq_gather_blocks`` launch and scattered on arrival by
+one ``kvq_scatter_blocks`` launch (native page-copy kernel).  Both are
+device-side copies, so the only host<->device traffic is the 16-byte header.
 """
 from __future__ import annotations
 
@@ -22,6 +22,7 @@ from typing import List, Optional, Sequence
 import torch
 import torch.distributed as dist
 
+from . import _lib
 from ._lib import PAGE_BYTES
 from .cache import BlockAllocator, PagedKVCache
 
@@ -31,17 +32,46 @@ def wire_bytes_per_token(num_kv_heads: int) -> int:
     return num_kv_heads * PAGE_BYTES // 16
 
 
+def _ids(block_ids, device) -> torch.Tensor:
+    """Block ids as a device int32 tensor (a device tensor passes through)."""
+    if isinstance(block_ids, torch.Tensor) and block_ids.is_cuda and block_ids.dtype == torch.int32:
+        return block_ids.contiguous()
+    import numpy as np
+    return torch.from_numpy(np.asarray(block_ids, dtype=np.int32)).to(device)
+
+
 def export_pages(cache: PagedKVCache, block_ids: Sequence[int]) -> torch.Tensor:
-    """``uint8[n, Hkv, 4224]`` copy of the given blocks' pages (all heads)."""
-    idx = torch.as_tensor(list(block_ids), dtype=torch.long, device=cache.device)
-    return cache.pool.index_select(0, idx)
+    """``uint8[n, Hkv, 4224]`` copy of the given blocks' pages (all heads):
+    ``kvq_gather_blocks`` on the device (the CPU-side tensors of the gloo
+    tests are copied by torch; there is no compute on this path)."""
+    n, hkv = len(block_ids), cache.spec.num_kv_heads
+    if not cache.pool.is_cuda:
+        return cache.pool.index_select(0, torch.as_tensor([int(b) for b in block_ids], dtype=torch.long))
+    out = torch.empty((n, hkv, PAGE_BYTES), dtype=torch.uint8, device=cache.device)
+    if n:
+        idx = _ids(block_ids, cache.device)
+        st = _lib.load().kvq_gather_blocks(cache.pool.data_ptr(), cache.num_blocks, hkv, idx.data_ptr(), n,
+                                           out.data_ptr(), torch.cuda.current_stream(cache.device).cuda_stream)
+        _lib.check("kvq_gather_blocks", st)
+    return out
 
 
 def import_pages(cache: PagedKVCache, block_ids: Sequence[int], pages: torch.Tensor) -> None:
+    """Scatter a packed page buffer into the given blocks (``kvq_scatter_blocks``)."""
     if pages.shape[1:] != cache.pool.shape[1:] or pages.shape[0] != len(block_ids):
         raise ValueError("page buffer does not match the destination pool")
-    idx = torch.as_tensor(list(block_ids), dtype=torch.long, device=cache.device)
-    cache.pool.index_copy_(0, idx, pages)
+    if not cache.pool.is_cuda:
+        cache.pool.index_copy_(0, torch.as_tensor([int(b) for b in block_ids], dtype=torch.long), pages)
+        return
+    if not pages.is_cuda or not pages.is_contiguous() or pages.dtype != torch.uint8:
+        raise ValueError("import_pages: pages must be a contiguous uint8 CUDA tensor")
+    n = len(block_ids)
+    if n:
+        idx = _ids(block_ids, cache.device)
+        st = _lib.load().kvq_scatter_blocks(cache.pool.data_ptr(), cache.num_blocks, cache.spec.num_kv_heads,
+                                            idx.data_ptr(), n, pages.data_ptr(),
+                                            torch.cuda.current_stream(cache.device).cuda_stream)
+        _lib.check("kvq_scatter_blocks", st)
 
 
 def send_sequence(cache: PagedKVCache, alloc: BlockAllocator, seq_id, dst: int,

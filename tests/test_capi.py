@@ -18,7 +18,7 @@ def declared_functions():
 
 def test_header_matches_binding():
     names = declared_functions()
-    assert len(names) == 17
+    assert len(names) == 19
     assert set(names) == set(_lib.SIGNATURES)
 
 

@@ -7,7 +7,8 @@ import torch
 
 import oracle as O
 from kvq_testutil import bf16_bits, make_kv, make_q
-from paper_2605_29639_b200 import KVCacheSpec, PagedKVCache, paged_decode_attention, quantize_append
+from paper_2605_29639_b200 import (KVCacheSpec, PagedKVCache, copy_blocks, paged_decode_attention,
+                                   quantize_append)
 from paper_2605_29639_b200.prefix import PrefixKVCache
 from paper_2605_29639_b200.transfer import export_pages, import_pages
 
@@ -51,3 +52,27 @@ def test_export_import_pages(cuda):
     import_pages(dst, [0, 5, 9], pages)
     for s, d in ((3, 0), (7, 5), (1, 9)):
         assert torch.equal(src.pool[s], dst.pool[d])
+
+
+@pytest.mark.parametrize("Hkv", [1, 3, 8])
+def test_gather_scatter_blocks_native(cuda, Hkv):
+    """kvq_gather_blocks / kvq_scatter_blocks (the PD wire format) and the
+    copy-on-write kvq_copy_blocks move whole blocks bit for bit, for odd head
+    counts and many blocks; out-of-range ids are skipped."""
+    nb = 700
+    src = PagedKVCache(KVCacheSpec(Hkv), nb, device=cuda)
+    src.pool.random_(0, 256)
+    rng = np.random.default_rng(Hkv)
+    ids = rng.permutation(nb)[:500].tolist()
+    pages = export_pages(src, ids)
+    assert torch.equal(pages, src.pool[torch.as_tensor(ids, device=cuda)])
+    dst = PagedKVCache(KVCacheSpec(Hkv), nb, device=cuda)
+    dids = rng.permutation(nb)[:500].tolist()
+    import_pages(dst, dids, pages)
+    assert torch.equal(dst.pool[torch.as_tensor(dids, device=cuda)], pages)
+    untouched = sorted(set(range(nb)) - set(dids))
+    assert int(dst.pool[torch.as_tensor(untouched, device=cuda)].count_nonzero()) == 0
+    before = dst.pool.clone()
+    copy_blocks(dst, [(dids[0], dids[1]), (nb + 5, dids[2])])       # second pair is out of range: skipped
+    torch.cuda.synchronize()
+    assert torch.equal(dst.pool[dids[1]], before[dids[0]]) and torch.equal(dst.pool[dids[2]], before[dids[2]])

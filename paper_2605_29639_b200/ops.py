@@ -97,7 +97,8 @@ def paged_decode_attention(q: torch.Tensor, cache: PagedKVCache, block_table: to
                            total_pages: Optional[int] = None,
                            out: Optional[torch.Tensor] = None,
                            out_dtype: torch.dtype = torch.bfloat16, head_major: bool = False,
-                           workspace: Optional[torch.Tensor] = None) -> torch.Tensor:
+                           workspace: Optional[torch.Tensor] = None,
+                           num_splits: Optional[int] = None) -> torch.Tensor:
     """GQA decode attention of one query token per sequence over the paged,
     quantized KV cache -- or, with ``q`` of shape ``[B, q_len, Hq, 128]``, of
     ``q_len`` new tokens per sequence (speculative scoring / MTP), causal
@@ -108,7 +109,9 @@ def paged_decode_attention(q: torch.Tensor, cache: PagedKVCache, block_table: to
     seq_lens: int32 ``[B]``.  Returns ``[B, Hq, 128]`` (or ``[Hq, B, 128]``
     with ``head_major=True``, the layout the KV-head all-gather wants) in
     ``out_dtype`` (bf16 or fp32).  ``total_pages`` (sum of per-sequence
-    pages, when the host knows it) sharpens the split-KV geometry."""
+    pages, when the host knows it) sharpens the split-KV geometry;
+    ``num_splits`` (SURVEY §8b's name) instead fixes the split count of the
+    longest sequence: ``pages_per_split = ceil(max_blocks / num_splits)``."""
     _require_cuda("paged_decode_attention", q, block_table, seq_lens, cache.pool)
     spec = cache.spec
     multi = q.dim() == 4  # [B, q_len, Hq, 128]: speculative scoring / MTP (causal among the new tokens)
@@ -139,6 +142,10 @@ def paged_decode_attention(q: torch.Tensor, cache: PagedKVCache, block_table: to
     if sm_scale is None:
         sm_scale = 1.0 / math.sqrt(128)
     lib = _lib.load()
+    if num_splits is not None:
+        if pages_per_split is not None or num_splits < 1:
+            raise ValueError("paged_decode_attention: give num_splits >= 1 or pages_per_split, not both")
+        pages_per_split = -(-max_blocks // int(num_splits))
     pps = pages_per_split or lib.kvq_decode_pages_per_split(
         B, spec.num_kv_heads, total_pages if total_pages is not None else B * max_blocks, max_blocks)
     max_splits = -(-max_blocks // pps)

@@ -71,6 +71,10 @@ def test_split_invariance(cuda, pps):
     assert rel_err(out, ref) <= 2e-3
     base = gpu_attn(sc, cuda, out_dtype=torch.float32, pages_per_split=1000)
     assert rel_err(out, base) <= 2e-3  # fp16 P rounding differs with the split geometry
+    if pps in (7, 32):  # num_splits is the same geometry expressed as a split count
+        ns = -(-sc.max_blocks // pps)
+        assert np.array_equal(gpu_attn(sc, cuda, out_dtype=torch.float32, num_splits=ns),
+                              gpu_attn(sc, cuda, out_dtype=torch.float32, pages_per_split=-(-sc.max_blocks // ns)))
 
 
 def test_empty_and_head_major(cuda):

@@ -610,26 +610,35 @@ def run_c5(args, cfg):
     def k2():
         paged_decode_attention(q, cache, table, lens_d, out=out, pages_per_split=pps, workspace=ws)
 
-    k1(); k2(); torch.cuda.synchronize()
+    def step():  # kvq_decode_step: K1 over all appended rows, K2 PDL-launched behind it
+        ops.decode_step(cache, kv_step[0], kv_step[1], slots_step, q, table, lens_d, out=out,
+                        pages_per_split=pps, workspace=ws)
+
+    k1(); k2(); step(); torch.cuda.synchronize()
     graphs = []
-    for fn in (k1, k2):
+    for fn in (k1, k2, step):
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g):
             fn()
         graphs.append(g)
+    g_k1, g_k2, g_step = graphs
     for _ in range(args.warmup):
-        graphs[0].replay(); graphs[1].replay()
+        g_step.replay()
     torch.cuda.synchronize()
-    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
     sampler = ClockSampler(0)
     with sampler:
         t0 = torch.cuda.Event(enable_timing=True); t1 = torch.cuda.Event(enable_timing=True)
         t0.record()
         for i in range(args.steps):
-            ev[i][0].record(); graphs[0].replay(); ev[i][1].record(); graphs[1].replay(); ev[i][2].record()
+            g_step.replay()
         t1.record()
         torch.cuda.synchronize()
     ms_step = t0.elapsed_time(t1) / args.steps
+    # per-kernel breakdown (separate graphs, no PDL): K1 and K2 each bracketed by events
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
+    for i in range(args.steps):
+        ev[i][0].record(); g_k1.replay(); ev[i][1].record(); g_k2.replay(); ev[i][2].record()
+    torch.cuda.synchronize()
     k1_ms = statistics.mean(e[0].elapsed_time(e[1]) for e in ev)
     k2_ms = statistics.mean(e[1].elapsed_time(e[2]) for e in ev)
 

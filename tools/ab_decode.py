@@ -14,7 +14,7 @@ import sys
 import numpy as np
 import torch
 
-SHAPES = {"c1": (8, 32, 8, 2048, 0), "c2": (256, 32, 8, "ragged", 0), "c3": (128, 64, 8, 32768, 1), "c4": (64, 64, 4, 131072, 0)}
+SHAPES = {"c2f": (256, 32, 8, "ragged", 1), "c3i": (128, 64, 8, 32768, 0), "c2e": (256, 32, 8, 4352, 0), "c1": (8, 32, 8, 2048, 0), "c2": (256, 32, 8, "ragged", 0), "c3": (128, 64, 8, 32768, 1), "c4": (64, 64, 4, 131072, 0)}
 
 
 def main():

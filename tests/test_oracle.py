@@ -1,7 +1,8 @@
 """The CPU oracle pinned before it is trusted: contract KATs (hand-derived and
 cross-checked with third-party FP8 encoders), agreement of the two independent
-restatements (C and numpy), page-layout round trips, and attention properties
-(split-KV invariance, GQA == repeated-KV MHA, dequantisation error bounds)."""
+restatements (C and numpy), page-layout round trips, attention properties
+(split-KV invariance, GQA == repeated-KV MHA, dequantisation error bounds) and
+the attention math against PyTorch's scaled_dot_product_attention."""
 import json
 import math
 from pathlib import Path
@@ -145,3 +146,24 @@ def test_oracle_threads_deterministic():
     a = O.decode_attn(bf16_bits(sc.q), sc.pool, sc.block_table, sc.seq_lens, 8, O.FP8_E4M3, nthreads=1)
     b = O.decode_attn(bf16_bits(sc.q), sc.pool, sc.block_table, sc.seq_lens, 8, O.FP8_E4M3, nthreads=8)
     assert np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("kv_dtype", [O.INT8, O.FP8_E4M3])
+def test_attention_oracle_matches_torch_sdpa(kv_dtype):
+    """The attention oracle against an independent implementation: PyTorch's
+    scaled_dot_product_attention (fp64, GQA via enable_gqa) over the same
+    dequantized K/V (code * scale, read back through the page layout).  This
+    pins the oracle's softmax / GQA / masking math to third-party code; the
+    quantizer is pinned by the KATs above."""
+    from kvq_testutil import Scenario, bf16_bits
+    Hq, Hkv = 32, 8
+    sc = Scenario([1, 15, 16, 17, 300, 1029], Hq, Hkv, kv_dtype, seed=12)
+    ref = O.decode_attn(bits := bf16_bits(sc.q), sc.pool, sc.block_table, sc.seq_lens, Hkv, kv_dtype)
+    kd, vd = _dense(sc.pool, sc.block_table, sc.seq_lens, kv_dtype)   # [B, Hkv, T, d]
+    q = torch.from_numpy(O.bf16_bits_to_f32(bits)).double()             # [B, Hq, d]
+    for b, L in enumerate(sc.seq_lens):
+        k = torch.from_numpy(kd[b, :, :L]).double()[None]                # [1, Hkv, L, d]
+        v = torch.from_numpy(vd[b, :, :L]).double()[None]
+        o = torch.nn.functional.scaled_dot_product_attention(q[b][None, :, None], k, v, enable_gqa=True,
+                                                             scale=1.0 / math.sqrt(128))[0, :, 0]
+        assert np.abs(ref[b] - o.numpy()).max() <= 2e-6 * max(1.0, float(o.abs().max())), b

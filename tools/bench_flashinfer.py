@@ -1,0 +1,86 @@
+"""Library baseline: flashinfer's paged FP8-E4M3 decode attention on the C3
+workload (Qwen2.5-72B shape: Hq = 64, Hkv = 8, d = 128, B = 128, ctx 32K,
+page 16), next to libkvq's K2 on the same shape.  flashinfer reads 256 B per
+(token, kv head) (codes only, one scale per tensor); libkvq reads 264 B (codes
++ per-token scales).  Both timed as back-to-back launches with CUDA events.
+
+    python tools/bench_flashinfer.py [--steps K] [--tensor-cores]
+"""
+import argparse
+import json
+import math
+import sys
+from pathlib import Path
+
+import numpy as np
+import torch
+
+REPO = Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(REPO))
+
+
+def timed(fn, steps):
+    for _ in range(5):
+        fn()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(steps):
+        fn()
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / steps
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--tensor-cores", action="store_true")
+    args = ap.parse_args()
+    import flashinfer
+    from paper_2605_29639_b200 import KVCacheSpec, PagedKVCache, ops, paged_decode_attention
+    dev = torch.device("cuda:0")
+    B, Hq, Hkv, ctx = 128, 64, 8, 32769
+    npg = -(-ctx // 16)
+    NB = B * npg
+    perm = torch.from_numpy(np.random.default_rng(7).permutation(NB).astype(np.int32)).to(dev)
+    q = torch.randn((B, Hq, 128), device=dev).to(torch.bfloat16)
+    lines = []
+
+    # ---- flashinfer: paged KV [NB, 2, 16, Hkv, 128] fp8 (NHD), random block ids
+    kv = (torch.randn((NB, 2, 16, Hkv, 128), device=dev) * 40).to(torch.float8_e4m3fn)
+    indptr = torch.arange(0, B + 1, dtype=torch.int32, device=dev) * npg
+    last = torch.full((B,), ctx - (npg - 1) * 16, dtype=torch.int32, device=dev)
+    ws = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+    w = flashinfer.BatchDecodeWithPagedKVCacheWrapper(ws, "NHD", use_tensor_cores=args.tensor_cores)
+    w.plan(indptr, perm, last, Hq, Hkv, 128, 16, q_data_type=torch.bfloat16, kv_data_type=torch.float8_e4m3fn,
+           sm_scale=1.0 / math.sqrt(128))
+    out = torch.empty((B, Hq, 128), dtype=torch.bfloat16, device=dev)
+    t_fi = timed(lambda: w.run(q, kv, out=out, k_scale=0.0125, v_scale=0.03125), args.steps)
+    fi_bytes = B * ctx * Hkv * 256 + B * Hq * 512 + NB * 4
+    lines.append({"impl": "flashinfer " + flashinfer.__version__ + (" (tensor cores)" if args.tensor_cores else ""),
+                  "workload": "C3: B=128, ctx 32K, Hq=64, Hkv=8, FP8-E4M3 KV, page 16", "ms": t_fi,
+                  "gbs": fi_bytes / (t_fi * 1e-3) / 1e9, "tokens_per_s": B / (t_fi * 1e-3)})
+    del kv, w, ws
+    torch.cuda.empty_cache()
+
+    # ---- libkvq K2 on the same shape
+    pool = torch.randint(0, 256, (NB, Hkv, 4224), dtype=torch.uint8, device=dev)
+    pool[..., :4096] &= 0xF7
+    pool[..., 4096:] = torch.full((NB, Hkv, 32), 0.02, device=dev).view(torch.uint8).view(NB, Hkv, 128)
+    cache = PagedKVCache(KVCacheSpec(Hkv, kv_dtype="fp8_e4m3"), NB, device=dev, pool=pool)
+    table = perm.view(B, npg).contiguous()
+    lens = torch.full((B,), ctx, dtype=torch.int32, device=dev)
+    pps = ops.pages_per_split(B, Hkv, NB, npg)
+    o2 = torch.empty((B, Hq, 128), dtype=torch.bfloat16, device=dev)
+    t_k = timed(lambda: paged_decode_attention(q, cache, table, lens, out=o2, pages_per_split=pps), args.steps)
+    k_bytes = B * ctx * Hkv * 264 + B * Hq * 512 + NB * 4
+    lines.append({"impl": "libkvq K2", "workload": "C3: B=128, ctx 32K, Hq=64, Hkv=8, FP8-E4M3 KV (+ per-token scales)",
+                  "ms": t_k, "gbs": k_bytes / (t_k * 1e-3) / 1e9, "tokens_per_s": B / (t_k * 1e-3),
+                  "speedup_vs_flashinfer": t_fi / t_k})
+    for l in lines:
+        print(json.dumps(l), flush=True)
+
+
+if __name__ == "__main__":
+    main()

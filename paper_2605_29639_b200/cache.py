@@ -112,7 +112,7 @@ class PagedKVCache:
 # ---------------------------------------------------------------------------
 def _layout_index() -> Tuple[np.ndarray, np.ndarray]:
     """code_idx[kv, t, d] and scale_idx[kv, t]: byte offsets inside a page
-    (same formulas as kvq_kernels.cu k_code_off / v_code_off)."""
+    (same formulas as csrc/kvq_common.cuh k_code_off / v_code_off)."""
     code = np.zeros((2, BLOCK_SIZE, HEAD_DIM), dtype=np.int64)
     for t in range(BLOCK_SIZE):
         for d in range(HEAD_DIM):

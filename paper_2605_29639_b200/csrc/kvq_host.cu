@@ -1,5 +1,9 @@
-// kvq_host.cu -- host-side native helpers of libkvq (no device code).
+// kvq_host.cu -- host-side native parts of libkvq (no device code).
 //
+//   kvq_version / kvq_last_error / kvq_page_bytes: ABI identity and errors.
+//   kvq_pipeline_submit: the serving loop's per-step enqueue (upload, step
+//   graph, download) in one call.  kvq_sym_*: IPC-shareable buffers of the
+//   fused peer gather.
 //   kvq_block_hashes: chained 64-bit block keys for prefix reuse of quantized
 //   pages.  Same key definition as the reference's prefix-cache identity
 //   (servesim blocks.py:29-69: FNV-1a over 8-byte little-endian words; the
@@ -9,7 +13,7 @@
 //   the reference's frozen value, test_blocks.py:63-66).
 #include <stdint.h>
 
-#include "kvq.h"
+#include "kvq_common.cuh"
 
 namespace {
 constexpr uint64_t kFnvOffset = 0xCBF29CE484222325ull;
@@ -39,3 +43,84 @@ extern "C" int64_t kvq_block_hashes(const int64_t* tokens, int64_t n, int32_t bl
   }
   return nkeys;
 }
+
+// ---------------------------------------------------------------------------
+// Host runtime: version / error reporting, the serving loop's step submitter,
+// symmetric (IPC-shareable) buffers for the fused peer gather.
+// ---------------------------------------------------------------------------
+namespace kvq_abi {
+thread_local char g_err[512] = "";
+}
+using namespace kvq_abi;
+
+extern "C" {
+
+int kvq_version(void) { return KVQ_ABI_VERSION; }
+
+const char* kvq_last_error(void) { return g_err; }
+
+size_t kvq_page_bytes(void) { return KVQ_PAGE_BYTES; }
+
+int kvq_pipeline_submit(const kvq_pipe_step* s) {
+  if (!s || !s->graph_exec || !s->dev_in || !s->host_in || !s->dev_out || !s->host_out || !s->ev_in_ready ||
+      !s->ev_done || !s->ev_out_done)
+    return fail(KVQ_EINVAL, "pipeline_submit: null handle or buffer");
+  auto h2d = static_cast<cudaStream_t>(s->h2d_stream);
+  auto cmp = static_cast<cudaStream_t>(s->compute_stream);
+  auto d2h = static_cast<cudaStream_t>(s->d2h_stream);
+  auto in_ready = static_cast<cudaEvent_t>(s->ev_in_ready);
+  auto done = static_cast<cudaEvent_t>(s->ev_done);
+  auto out_done = static_cast<cudaEvent_t>(s->ev_out_done);
+  cudaError_t e = cudaSuccess;
+  auto ok = [&](cudaError_t r) { if (e == cudaSuccess) e = r; };
+  if (s->reuse) ok(cudaStreamWaitEvent(h2d, done, 0));      // the slot's previous kernels read dev_in
+  ok(cudaMemcpyAsync(s->dev_in, s->host_in, s->in_bytes, cudaMemcpyHostToDevice, h2d));
+  ok(cudaEventRecord(in_ready, h2d));
+  ok(cudaStreamWaitEvent(cmp, in_ready, 0));
+  if (s->reuse) ok(cudaStreamWaitEvent(cmp, out_done, 0));  // the slot's previous download read dev_out
+  ok(cudaGraphLaunch(static_cast<cudaGraphExec_t>(s->graph_exec), cmp));
+  ok(cudaEventRecord(done, cmp));
+  ok(cudaStreamWaitEvent(d2h, done, 0));
+  ok(cudaMemcpyAsync(s->host_out, s->dev_out, s->out_bytes, cudaMemcpyDeviceToHost, d2h));
+  ok(cudaEventRecord(out_done, d2h));
+  if (e != cudaSuccess) return fail(KVQ_ECUDA, cudaGetErrorString(e));
+  return KVQ_OK;
+}
+
+int kvq_sym_alloc(size_t bytes, void** ptr, void* ipc_handle) {
+  if (!ptr || !ipc_handle || bytes == 0) return fail(KVQ_EINVAL, "sym_alloc: bad arguments");
+  void* p = nullptr;
+  cudaError_t e = cudaMalloc(&p, bytes);
+  if (e == cudaSuccess) e = cudaMemset(p, 0, bytes);
+  cudaIpcMemHandle_t h;
+  if (e == cudaSuccess) e = cudaIpcGetMemHandle(&h, p);
+  if (e != cudaSuccess) {
+    if (p) cudaFree(p);
+    return fail(KVQ_ECUDA, cudaGetErrorString(e));
+  }
+  static_assert(sizeof(h) == KVQ_IPC_HANDLE_BYTES, "IPC handle size");
+  memcpy(ipc_handle, &h, sizeof(h));
+  *ptr = p;
+  return KVQ_OK;
+}
+
+int kvq_sym_open(const void* ipc_handle, void** ptr) {
+  if (!ptr || !ipc_handle) return fail(KVQ_EINVAL, "sym_open: bad arguments");
+  cudaIpcMemHandle_t h;
+  memcpy(&h, ipc_handle, sizeof(h));
+  const cudaError_t e = cudaIpcOpenMemHandle(ptr, h, cudaIpcMemLazyEnablePeerAccess);
+  if (e != cudaSuccess) return fail(KVQ_ECUDA, cudaGetErrorString(e));
+  return KVQ_OK;
+}
+
+int kvq_sym_close(void* ptr) {
+  const cudaError_t e = cudaIpcCloseMemHandle(ptr);
+  return e == cudaSuccess ? KVQ_OK : fail(KVQ_ECUDA, cudaGetErrorString(e));
+}
+
+int kvq_sym_free(void* ptr) {
+  const cudaError_t e = cudaFree(ptr);
+  return e == cudaSuccess ? KVQ_OK : fail(KVQ_ECUDA, cudaGetErrorString(e));
+}
+
+}  // extern "C"

@@ -319,6 +319,7 @@ class _Seq:
     hashing: bool = False                  # token ids known: full pages get prefix keys
     last_hash: int = 0                     # chain key of the last full page (0 = seed)
     tail_tokens: List[int] = field(default_factory=list)
+    blocks: List[int] = field(default_factory=list)  # physical block of each key (fixed while referenced)
 
 
 def block_hashes(tokens: Sequence[int], block_size: int = BLOCK_SIZE, prev_key: int = 0) -> List[int]:
@@ -374,7 +375,7 @@ class BlockAllocator:
         return 0 if e is None else e.watermark
 
     def block_ids(self, seq_id) -> List[int]:
-        return [self.pool.lookup(k) for k in self._seq(seq_id).keys]
+        return list(self._seq(seq_id).blocks)
 
     def seq_len(self, seq_id) -> int:
         return self._seq(seq_id).length
@@ -433,7 +434,9 @@ class BlockAllocator:
         pos = s.length
         while len(slots) < n:
             if pos % bs == 0:
-                s.keys.append(self._new_block())
+                key = self._new_block()
+                s.keys.append(key)
+                s.blocks.append(self.pool.entry(key).block)
             key = s.keys[pos // bs]
             e = self.pool.entry(key)
             take = min(n - len(slots), bs - pos % bs)
@@ -443,6 +446,33 @@ class BlockAllocator:
             self.pool.set_watermark(key, pos - (pos - 1) // bs * bs)
         s.length = pos
         return slots
+
+    def append_one(self, seq_ids: Sequence) -> np.ndarray:
+        """The decode step's slots: one new token for each of ``seq_ids`` (the
+        batched form of ``append_slots(s, 1)``, same rules); returns int32
+        ``block * 16 + offset`` per sequence.  Atomic: on
+        :class:`CacheThrashError` nothing changes."""
+        seqs = [self._seq(s) for s in seq_ids]
+        bs = self.block_size
+        need = sum(1 for s in seqs if s.length % bs == 0)
+        if need > self.num_available:
+            raise CacheThrashError((need - self.num_available) * self.bytes_per_block)
+        self.clock += 1
+        out = np.empty(len(seqs), dtype=np.int32)
+        entries = self.pool._entries
+        for i, s in enumerate(seqs):
+            off = s.length % bs
+            if off == 0:
+                key = self._new_block()
+                s.keys.append(key)
+                s.blocks.append(entries[key].block)
+            e = entries[s.keys[-1]]
+            if e.watermark > off + 1:  # the grow-only rule of set_watermark
+                raise ValueError("watermark may only grow, up to block_size")
+            e.watermark = off + 1
+            out[i] = s.blocks[-1] * bs + off
+            s.length += 1
+        return out
 
     def fork(self, parent_id, child_id) -> List[Tuple[int, int]]:
         """New sequence sharing the parent's full blocks; the partial tail is
@@ -466,7 +496,8 @@ class BlockAllocator:
             keys.append(dst)
             copies.append((self.pool.lookup(tail), self.pool.lookup(dst)))
         self._seqs[child_id] = _Seq(keys=keys, length=p.length, hashing=p.hashing,
-                                    last_hash=p.last_hash, tail_tokens=list(p.tail_tokens))
+                                    last_hash=p.last_hash, tail_tokens=list(p.tail_tokens),
+                                    blocks=[self.pool.lookup(k) for k in keys])
         return copies
 
     # -- prefix reuse (reference prefix identity blocks.py:51-69)
@@ -484,7 +515,7 @@ class BlockAllocator:
             key = ("h", h)
             if self.pool.entry(key) is None and not (promote is not None and promote(key)):
                 break
-            self.pool.acquire(key, self.clock)
+            s.blocks.append(self.pool.acquire(key, self.clock).block)
             s.keys.append(key)
             s.length += self.block_size
             s.last_hash = h
@@ -525,7 +556,7 @@ class BlockAllocator:
 
     # -- device views
     def block_table(self, seq_ids: Sequence, max_blocks: Optional[int] = None) -> np.ndarray:
-        rows = [self.block_ids(s) for s in seq_ids]
+        rows = [self._seq(s).blocks for s in seq_ids]
         mb = max_blocks if max_blocks is not None else max([len(r) for r in rows] + [1])
         out = np.zeros((len(rows), mb), dtype=np.int32)
         for i, r in enumerate(rows):
@@ -542,6 +573,7 @@ class BlockAllocator:
         counts: Dict[object, int] = {}
         for s in self._seqs.values():
             assert len(s.keys) == -(-s.length // self.block_size), "block count vs length"
+            assert s.blocks == [self.pool.lookup(k) for k in s.keys], "cached block ids"
             for i, k in enumerate(s.keys):
                 counts[k] = counts.get(k, 0) + 1
                 full = (i + 1) * self.block_size <= s.length
@@ -567,30 +599,47 @@ class BlockAllocator:
 
 class BlockTable:
     """Device-resident ``int32[max_seqs, max_blocks]`` table plus ``seq_lens``,
-    updated incrementally (only changed entries cross host->device)."""
+    updated incrementally: each row remembers which sequence it holds and how
+    many of its block ids are already on the device, so a decode step moves
+    only the block ids appended since the last sync (a few per step) and the
+    lengths, instead of rebuilding the table."""
 
     def __init__(self, max_seqs: int, max_blocks: int, device="cuda"):
         self.max_seqs, self.max_blocks = max_seqs, max_blocks
         self.table = torch.zeros((max_seqs, max_blocks), dtype=torch.int32, device=device)
         self.seq_lens = torch.zeros((max_seqs,), dtype=torch.int32, device=device)
-        self._host = np.zeros((max_seqs, max_blocks), dtype=np.int32)
+        self._row_seq: List[object] = [None] * max_seqs   # the _Seq a row holds
+        self._row_n = np.zeros((max_seqs,), dtype=np.int64)  # its block ids already on the device
         self._host_lens = np.zeros((max_seqs,), dtype=np.int32)
 
     def sync(self, alloc: BlockAllocator, seq_ids: Sequence) -> int:
         """Push the rows of ``seq_ids`` (row i <- seq_ids[i]); returns the
         number of table entries transferred."""
-        tab = alloc.block_table(seq_ids, self.max_blocks)
-        lens = alloc.seq_lens(seq_ids)
         n = len(seq_ids)
-        diff = np.nonzero(tab != self._host[:n])
-        moved = 0
-        if diff[0].size:
-            upd = np.stack([diff[0], diff[1], tab[diff]], axis=1).astype(np.int64)
-            u = torch.from_numpy(upd).to(self.table.device, non_blocking=False)
-            self.table[u[:, 0], u[:, 1]] = u[:, 2].to(torch.int32)
-            self._host[:n] = tab
-            moved = int(diff[0].size)
+        if n > self.max_seqs:
+            raise ValueError("more sequences than table rows")
+        rows, cols, vals = [], [], []
+        lens = np.empty((n,), dtype=np.int32)
+        for i, sid in enumerate(seq_ids):
+            s = alloc._seq(sid)
+            if self._row_seq[i] is not s:       # row now holds another sequence: rewrite it
+                self._row_seq[i] = s
+                self._row_n[i] = 0
+            b = s.blocks
+            k0 = int(self._row_n[i])
+            if len(b) > k0:
+                if len(b) > self.max_blocks:
+                    raise ValueError("max_blocks too small")
+                rows.extend([i] * (len(b) - k0))
+                cols.extend(range(k0, len(b)))
+                vals.extend(b[k0:])
+                self._row_n[i] = len(b)
+            lens[i] = s.length
+        if rows:
+            upd = torch.from_numpy(np.array([rows, cols, vals], dtype=np.int64))
+            upd = upd.to(self.table.device, non_blocking=False)
+            self.table[upd[0], upd[1]] = upd[2].to(torch.int32)
         if not np.array_equal(lens, self._host_lens[:n]):
             self.seq_lens[:n].copy_(torch.from_numpy(lens))
             self._host_lens[:n] = lens
-        return moved
+        return len(rows)

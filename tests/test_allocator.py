@@ -157,3 +157,67 @@ def test_random_ops_shadow_model(seed):
             ids = a.block_ids(s)
             for pos in range(0, L, 7):
                 assert ids[pos // 16] * 16 + pos % 16 == slot_of[(s, pos)]
+
+
+@pytest.mark.parametrize("seed", [0, 1, 2])
+def test_decode_step_fast_paths(seed):
+    """append_one (the decode step's batched slots) == append_slots(s, 1) per
+    sequence, and the incremental BlockTable stays equal to a full rebuild
+    under joins, leaves, forks and prefills between steps."""
+    import numpy as np
+    from paper_2605_29639_b200.cache import BlockTable
+    rng = random.Random(seed)
+    a, b = BlockAllocator(600), BlockAllocator(600)      # a: fast paths, b: reference calls
+    table = BlockTable(24, 64, device="cpu")
+    live, nxt = [], 0
+    for step in range(120):
+        op = rng.random()
+        if op < 0.2 or len(live) < 4:                   # join with a prefill
+            n = rng.randint(0, 70)
+            for x in (a, b):
+                x.allocate(nxt)
+                x.append_slots(nxt, n)
+            live.append(nxt)
+            nxt += 1
+        elif op < 0.3:                                  # leave
+            s = live.pop(rng.randrange(len(live)))
+            a.free(s)
+            b.free(s)
+        elif op < 0.4:                                  # fork
+            p = rng.choice(live)
+            ca, cb = a.fork(p, nxt), b.fork(p, nxt)
+            assert ca == cb
+            live.append(nxt)
+            nxt += 1
+        live = live[:24]
+        for s in list(a.seq_ids()):
+            if s not in live:
+                a.free(s)
+                b.free(s)
+        rng.shuffle(live)                               # rows move between sequences
+        got = a.append_one(live)
+        want = [b.append_slots(s, 1)[0] for s in live]
+        assert got.tolist() == want
+        table.sync(a, live)
+        mb = 64
+        full = a.block_table(live, mb)
+        lens = a.seq_lens(live)
+        dev = table.table.numpy()[: len(live)]
+        for i, s in enumerate(live):
+            n = -(-int(lens[i]) // 16)
+            assert np.array_equal(dev[i, :n], full[i, :n]), (step, s)
+        assert np.array_equal(table.seq_lens.numpy()[: len(live)], lens)
+        a.check_invariants()
+        assert a.block_table(live, mb).tolist() == b.block_table(live, mb).tolist()
+
+
+def test_append_one_is_atomic_on_thrash():
+    a = BlockAllocator(4)
+    for s in range(4):
+        a.allocate(s)
+        a.append_slots(s, 16)                           # every block full: next token needs a new block
+    before = [a.seq_len(s) for s in range(4)]
+    with pytest.raises(CacheThrashError):
+        a.append_one([0, 1, 2, 3])
+    assert [a.seq_len(s) for s in range(4)] == before
+    a.check_invariants()

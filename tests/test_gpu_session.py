@@ -206,3 +206,51 @@ def test_native_pipeline_back_to_back(cuda):
     assert all("pipe" in b for b in sess.bufs), "native submitter not used"
     for a, b in zip(refs, outs):
         assert torch.equal(a, b)
+
+
+def test_serving_loop_growing_sequences(cuda):
+    """A decode loop as a server runs it: every step BlockAllocator.append_one
+    picks each sequence's slot (new pages across block boundaries), the
+    incremental BlockTable pushes only the new block ids into the device table
+    the captured graphs read, and DecodeSession(graphs=True) runs the step
+    from staged host inputs.  Each step's download equals direct op calls on
+    a second cache fed the same rows."""
+    from paper_2605_29639_b200 import BlockAllocator, BlockTable
+    B, Hq, Hkv, steps = 6, 32, 8, 40
+    alloc = BlockAllocator(400)
+    g = torch.Generator().manual_seed(11)
+    lens0 = [5, 16, 31, 100, 1, 250]
+    ca = PagedKVCache(KVCacheSpec(Hkv), 400, device=cuda)
+    cb = PagedKVCache(KVCacheSpec(Hkv), 400, device=cuda)
+    for s, n in enumerate(lens0):                      # prefill
+        alloc.allocate(s)
+        sl = torch.tensor(alloc.append_slots(s, n), dtype=torch.int32, device=cuda)
+        k = torch.randn((n, Hkv, 128), generator=g).to(torch.bfloat16).to(cuda)
+        v = torch.randn((n, Hkv, 128), generator=g).to(torch.bfloat16).to(cuda)
+        quantize_append(ca, k, v, sl)
+        quantize_append(cb, k, v, sl)
+    seqs = list(range(B))
+    table = BlockTable(B, 64, device=cuda)
+    table.sync(alloc, seqs)
+    sess = DecodeSession(ca, table.table, B, Hq, graphs=True, pages_per_split=4)
+    outs, refs = [], []
+    for step in range(steps):
+        slots = torch.from_numpy(alloc.append_one(seqs))
+        table.sync(alloc, seqs)                          # new pages land in the captured table
+        lens = torch.from_numpy(alloc.seq_lens(seqs))
+        q = torch.randn((B, Hq, 128), generator=g).to(torch.bfloat16)
+        k = torch.randn((B, Hkv, 128), generator=g).to(torch.bfloat16)
+        v = torch.randn((B, Hkv, 128), generator=g).to(torch.bfloat16)
+        h = sess.next_inputs()
+        for name, t in (("q", q), ("k", k), ("v", v), ("slots", slots), ("lens", lens)):
+            h[name].copy_(t)
+        o = torch.empty((B, Hq, 128), dtype=torch.bfloat16, pin_memory=True)
+        sess.submit_staged(o)
+        outs.append(o)
+        quantize_append(cb, k.to(cuda), v.to(cuda), slots.to(cuda))
+        refs.append(paged_decode_attention(q.to(cuda), cb, table.table, lens.to(cuda), pages_per_split=4).cpu())
+        sess.synchronize()                               # the table is edited on the host between steps
+    for a, b in zip(outs, refs):
+        assert torch.equal(a, b)
+    assert torch.equal(ca.pool, cb.pool)
+    alloc.check_invariants()

@@ -315,9 +315,10 @@ def run_ours(args, cfg):
             print(f"[bench] fused peer gather unavailable ({e}); NCCL all-gather", file=sys.stderr)
             gather_mode = f"nccl (peer setup failed: {type(e).__name__})"
     use_nccl = world > 1 and peer is None
+    # The stationary step re-appends each sequence's newest token (its last page).
     sess = DecodeSession(cache, table_d, B_loc, Hq_loc, total_pages=total_pages, head_major=True,
                          gather_factory=make_gather if use_nccl else None, peer=peer,
-                         pages_per_split=args.pages_per_split)
+                         pages_per_split=args.pages_per_split, append_tail_only=True)
     buf = sess.device_buffers(0)
     for name, t in (("q", q), ("k", k_new), ("v", v_new), ("slots", slots_step), ("lens", seq_lens_d)):
         buf[name].copy_(t)
@@ -427,7 +428,8 @@ def run_ours(args, cfg):
     # staging blobs once; every step still uploads them.
     es = DecodeSession(cache, table_d, B_loc, Hq_loc, total_pages=total_pages, head_major=True,
                        gather_factory=make_gather if use_nccl else None, peer=peer,
-                       pages_per_split=args.pages_per_split, graphs=not (one_gpu and use_nccl))
+                       pages_per_split=args.pages_per_split, graphs=not (one_gpu and use_nccl),
+                       append_tail_only=True)
     host_inputs = {"q": q, "k": k_new, "v": v_new, "slots": slots_step, "lens": seq_lens_d}
     for b in es.bufs:
         for name, t in host_inputs.items():
@@ -503,7 +505,8 @@ def run_ours(args, cfg):
                    if cache.nbytes() * world > 4 * 126e6 else "pool fits in L2: L2-resident numbers",
                    "step": "K1 append of B rows + K2 paged decode attention (+ the gather if N>1); "
                            "stationary ctx; the K timed steps are one CUDA graph (kvq_decode_step per step: K2 "
-                           "launched behind K1 with programmatic dependent launch, unrolled); K2 launch time "
+                           "launched behind K1 with programmatic dependent launch, waiting for K1 only before "
+                           "each sequence's last page; unrolled); K2 launch time "
                            "from event nodes around every k2_sample_every-th K2 (those steps launch K1, K2 plainly)",
                    "e2e": "DecodeSession(graphs=True).submit_staged: one H2D of the pinned q/k/v/slots/lens "
                           "staging blob, graph of K1, K2 (, all-gather), D2H of O; double-buffered copy "
@@ -610,9 +613,11 @@ def run_c5(args, cfg):
     def k2():
         paged_decode_attention(q, cache, table, lens_d, out=out, pages_per_split=pps, workspace=ws)
 
-    def step():  # kvq_decode_step: K1 over all appended rows, K2 PDL-launched behind it
+    def step():  # kvq_decode_step: K1 over all appended rows, K2 PDL-launched behind it; the
+        # prefill chunks belong to sequences K2 does not attend and each decode row is its
+        # sequence's newest token, so K2 streams all but the last pages while K1 runs
         ops.decode_step(cache, kv_step[0], kv_step[1], slots_step, q, table, lens_d, out=out,
-                        pages_per_split=pps, workspace=ws)
+                        pages_per_split=pps, workspace=ws, append_tail_only=True)
 
     k1(); k2(); step(); torch.cuda.synchronize()
     graphs = []

@@ -177,15 +177,21 @@ int kvq_decode_attn_peer(const void* q, int64_t q_batch_stride, const void* pool
  * block-table and barrier setup) overlap K1, and it waits for K1
  * (griddepcontrol.wait) before reading any page.  Valid because K1 writes
  * only pages; q, block_table and seq_lens must be ready when the call is
- * enqueued, as for any stream-ordered call.  Replaces the decode-step pair
- * the reference charges as one constant, simulator.py:499-517. */
+ * enqueued, as for any stream-ordered call.  With flags & KVQ_STEP_APPEND_TAIL_ONLY
+ * the caller promises that, for every sequence K2 attends, the appended rows lie
+ * in its last page (a decode step's new token; rows of sequences K2 does not
+ * attend, e.g. chunked-prefill chunks, may go anywhere): K2 then streams every
+ * other page while K1 runs and waits for K1 only before each last page.
+ * Replaces the decode-step pair the reference charges as one constant,
+ * simulator.py:499-517. */
+#define KVQ_STEP_APPEND_TAIL_ONLY 1
 int kvq_decode_step(const void* k, const void* v, int64_t k_token_stride, int64_t v_token_stride,
                     const int32_t* slot_mapping, int32_t T, const void* q, int64_t q_batch_stride,
                     void* pool, int64_t num_blocks, const int32_t* block_table, int32_t max_blocks,
                     const int32_t* seq_lens, int32_t B, int32_t Hq, int32_t Hkv, int32_t kv_dtype,
                     float sm_scale, int32_t pages_per_split, void* workspace, size_t workspace_bytes,
                     void* out, int32_t out_dtype, int32_t out_layout, const kvq_peer_out* peer,
-                    void* stream);
+                    int32_t flags, void* stream);
 
 /* Host-side step submission of a double-buffered serving pipeline, in one
  * native call instead of ~10 runtime calls from the host language: upload the

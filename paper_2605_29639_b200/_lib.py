@@ -17,6 +17,7 @@ KVQ_OK, KVQ_EINVAL, KVQ_EUNSUPPORTED, KVQ_ECUDA = 0, -1, -2, -3
 KVQ_INT8, KVQ_FP8_E4M3 = 0, 1
 KVQ_OUT_BF16, KVQ_OUT_F32 = 0, 1
 KVQ_OUT_BHD, KVQ_OUT_HBD = 0, 1
+KVQ_STEP_APPEND_TAIL_ONLY = 1
 HEAD_DIM = 128
 BLOCK_SIZE = 16
 PAGE_BYTES = 4224
@@ -43,7 +44,8 @@ SIGNATURES = {
     "kvq_decode_attn_peer": (_c.c_int, [_vp, _i64, _vp, _i64, _vp, _i32, _vp, _i32, _i32, _i32, _i32,
                                         _f32, _i32, _vp, _sz, _vp, _vp]),
     "kvq_decode_step": (_c.c_int, [_vp, _vp, _i64, _i64, _vp, _i32, _vp, _i64, _vp, _i64, _vp, _i32, _vp,
-                                   _i32, _i32, _i32, _i32, _f32, _i32, _vp, _sz, _vp, _i32, _i32, _vp, _vp]),
+                                   _i32, _i32, _i32, _i32, _f32, _i32, _vp, _sz, _vp, _i32, _i32, _vp, _i32,
+                                   _vp]),
     "kvq_pipeline_submit": (_c.c_int, [_vp]),
     "kvq_sym_alloc": (_c.c_int, [_sz, _c.POINTER(_vp), _vp]),
     "kvq_sym_open": (_c.c_int, [_vp, _c.POINTER(_vp)]),

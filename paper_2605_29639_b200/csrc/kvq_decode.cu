@@ -29,6 +29,7 @@ struct DecodeParams {
   void* out;
   int out_f32, out_hbd;
   kvq_peer_out peer;    // n_peers == 0: local output only (no fused gather)
+  int tail_only;        // behind K1 (PDL): K1's rows lie only in each sequence's last page
 };
 
 constexpr int NW = 4;  // warps per CTA; every warp streams its own pages
@@ -199,6 +200,7 @@ struct PageStream {
   uint64_t policy;
   int cur, nxt;            // block ids of pages [base, base+32) and [base+32, base+64) (lane-parallel)
   int base;
+  int wait_j;              // page whose copy must wait for K1 (griddepcontrol.wait), or -1
 
   __device__ __forceinline__ int load_ids(int j0, int lane) const {
     const int j = j0 + lane;
@@ -220,6 +222,7 @@ struct PageStream {
     }
     const int blk = __shfl_sync(FULL, cur, j - base);
     if (lane == 0) {
+      if (j == wait_j) asm volatile("griddepcontrol.wait;" ::: "memory");
       mbar_arrive_expect_tx(&full[s], PAGE);
       bulk_g2s(ring + s * PAGE, head_base + blk * blk_stride, PAGE, &full[s], policy);
     }
@@ -304,9 +307,18 @@ __device__ __forceinline__ void decode_cta(const DecodeParams& p, uint8_t* smem)
   __syncwarp();
   ps.init(lane);
   // Launched behind K1 with programmatic serialization (kvq_decode_step): the
-  // prologue above (q, block table, barriers) overlapped K1; pages may hold
-  // K1's rows, so wait for it here.  A no-op for an ordinary launch.
-  asm volatile("griddepcontrol.wait;" ::: "memory");
+  // prologue above (q, block table, barriers) overlapped K1.  Pages may hold
+  // K1's rows, so wait for it here -- or, when the caller promises that K1
+  // wrote only each sequence's last page (a decode step's new token), only
+  // before that one page's copy, so the rest of the sequence streams while K1
+  // runs.  A no-op for an ordinary launch.
+  ps.wait_j = -1;
+  if (!p.tail_only) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+  } else {
+    const int last = npages - 1 - pg0;  // split-local index of the sequence's last page
+    if (last >= 0 && last < n && last % NW == warp) ps.wait_j = last / NW;
+  }
 #pragma unroll 1
   for (int j = 0; j < S && j < ps.nj; ++j) ps.issue(j, lane, j);
 
@@ -855,7 +867,7 @@ static int decode_attn_impl(const void* q, int64_t q_batch_stride, int32_t q_len
                             const int32_t* seq_lens, int32_t B, int32_t Hq, int32_t Hkv, int32_t kv_dtype,
                             float sm_scale, int32_t pages_per_split, void* workspace,
                             size_t workspace_bytes, void* out, int32_t out_dtype, int32_t out_layout,
-                            const kvq_peer_out* peer, void* stream, bool pdl = false) {
+                            const kvq_peer_out* peer, void* stream, bool pdl = false, bool tail_only = false) {
   if (B < 0 || Hq <= 0 || Hkv <= 0 || max_blocks <= 0 || num_blocks <= 0 || q_len <= 0)
     return fail(KVQ_EINVAL, "decode_attn: bad sizes");
   if (B == 0) return KVQ_OK;
@@ -908,6 +920,7 @@ static int decode_attn_impl(const void* q, int64_t q_batch_stride, int32_t q_len
   prm.out_hbd = out_layout == KVQ_OUT_HBD;
   prm.peer = kvq_peer_out{};
   if (peer) prm.peer = *peer;
+  prm.tail_only = pdl && tail_only;
 
   const dim3 grid((unsigned)max_splits, (unsigned)Hkv, (unsigned)B);
   auto st = static_cast<cudaStream_t>(stream);
@@ -953,7 +966,8 @@ int kvq_decode_step(const void* k, const void* v, int64_t k_token_stride, int64_
                     const int32_t* seq_lens, int32_t B, int32_t Hq, int32_t Hkv, int32_t kv_dtype,
                     float sm_scale, int32_t pages_per_split, void* workspace, size_t workspace_bytes,
                     void* out, int32_t out_dtype, int32_t out_layout, const kvq_peer_out* peer,
-                    void* stream) {
+                    int32_t flags, void* stream) {
+  if (flags & ~KVQ_STEP_APPEND_TAIL_ONLY) return fail(KVQ_EINVAL, "decode_step: unknown flags");
   if (peer && (out_dtype != KVQ_OUT_BF16 || out_layout != KVQ_OUT_HBD))
     return fail(KVQ_EINVAL, "decode_step: the fused gather writes bf16 head-major rows");
   if (int rc = kvq_quant_append(k, v, k_token_stride, v_token_stride, slot_mapping, T, Hkv, kv_dtype, pool,
@@ -973,7 +987,7 @@ int kvq_decode_step(const void* k, const void* v, int64_t k_token_stride, int64_
   // its launch and prologue overlap K1 (K1 never writes q, the table or lens).
   return decode_attn_impl(q, q_batch_stride, 1, pool, num_blocks, block_table, max_blocks, seq_lens, B, Hq,
                           Hkv, kv_dtype, sm_scale, pages_per_split, workspace, workspace_bytes, out, out_dtype,
-                          out_layout, peer, stream, /*pdl=*/T > 0);
+                          out_layout, peer, stream, /*pdl=*/T > 0, (flags & KVQ_STEP_APPEND_TAIL_ONLY) != 0);
 }
 
 int kvq_decode_attn_mq(const void* q, int64_t q_batch_stride, int32_t q_len, const void* pool,

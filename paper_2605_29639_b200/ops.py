@@ -221,12 +221,18 @@ def decode_step(cache: PagedKVCache, k: torch.Tensor, v: torch.Tensor, slot_mapp
                 sm_scale: Optional[float] = None, pages_per_split: Optional[int] = None,
                 total_pages: Optional[int] = None, out: Optional[torch.Tensor] = None,
                 out_dtype: torch.dtype = torch.bfloat16, head_major: bool = False,
-                workspace: Optional[torch.Tensor] = None, peer=None, slot: int = 0) -> torch.Tensor:
+                workspace: Optional[torch.Tensor] = None, peer=None, slot: int = 0,
+                append_tail_only: bool = False) -> torch.Tensor:
     """One decode step in one call (``kvq_decode_step``): :func:`quantize_append`
     of the new rows, then :func:`paged_decode_attention` (or, with ``peer``,
     :func:`paged_decode_attention_gathered`), with K2 launched behind K1 by
     programmatic dependent launch so its launch and prologue overlap K1.
-    Same arguments and results as the two calls in sequence."""
+    Same arguments and results as the two calls in sequence.
+
+    ``append_tail_only=True`` promises that, for every attended sequence, the
+    appended rows lie in its last page (true of a decode step's new token;
+    rows of sequences not in ``q``, e.g. prefill chunks, may go anywhere):
+    K2 then streams all other pages while K1 runs."""
     _check_append("decode_step", cache, k, v, slot_mapping)
     _require_cuda("decode_step", q, block_table, seq_lens)
     spec = cache.spec
@@ -272,7 +278,8 @@ def decode_step(cache: PagedKVCache, k: torch.Tensor, v: torch.Tensor, slot_mapp
         seq_lens.data_ptr(), B, Hq, spec.num_kv_heads, spec.kv_dtype_id, float(sm_scale), int(pps),
         workspace.data_ptr(), workspace.numel() * workspace.element_size(), out.data_ptr(),
         _lib.KVQ_OUT_F32 if out_dtype == torch.float32 else _lib.KVQ_OUT_BF16,
-        _lib.KVQ_OUT_HBD if head_major else _lib.KVQ_OUT_BHD, desc, _stream_handle(q.device))
+        _lib.KVQ_OUT_HBD if head_major else _lib.KVQ_OUT_BHD, desc,
+        _lib.KVQ_STEP_APPEND_TAIL_ONLY if append_tail_only else 0, _stream_handle(q.device))
     _lib.check("kvq_decode_step", st)
     return out
 

@@ -35,7 +35,7 @@ class DecodeSession:
                  *, total_pages: Optional[int] = None, out_dtype: torch.dtype = torch.bfloat16,
                  head_major: bool = False, sm_scale: Optional[float] = None, depth: int = 2,
                  gather_factory=None, pages_per_split: Optional[int] = None, graphs: bool = False,
-                 peer=None):
+                 peer=None, append_tail_only: bool = False):
         """With ``gather_factory`` (returning a
         :class:`paper_2605_29639_b200.shard.OutputGather`, one per buffer slot,
         for KV-head / 2-D sharding) the local head-major output
@@ -46,6 +46,10 @@ class DecodeSession:
         with ``slots >= depth``) the gather is fused into K2 instead: each
         buffer slot's K2 stores its rows into every rank's copy of the global
         output over peer memory, and the download reads the slot's copy.
+
+        ``append_tail_only=True`` promises that each step's slots are the
+        sequences' newest tokens (in their last page): K2 then streams every
+        other page while K1 runs (``ops.decode_step``).
 
         With ``graphs=True`` each buffer slot's device work (K1, K2 and the
         gather) is captured once as a CUDA graph on first use and replayed by
@@ -104,6 +108,7 @@ class DecodeSession:
                 gather=gather_factory() if gather_factory is not None else None, used=False, idx=i))
         self.step_idx = 0
         self.graphs = graphs
+        self.append_tail_only = append_tail_only
 
     def k1(self, buf) -> None:
         """Quantize-on-append of the step's new K/V rows (device buffers)."""
@@ -128,7 +133,7 @@ class DecodeSession:
         decode_step(self.cache, buf["k"], buf["v"], buf["slots"], buf["q"], self.block_table, buf["lens"],
                     sm_scale=self.sm_scale, pages_per_split=self.pps, out=buf["out"],
                     out_dtype=self.out_dtype, head_major=self.head_major, workspace=buf["ws"],
-                    peer=self.peer, slot=buf["idx"])
+                    peer=self.peer, slot=buf["idx"], append_tail_only=self.append_tail_only)
 
     def _kernels(self, buf, k1: bool = True) -> None:
         if k1:

@@ -127,8 +127,9 @@ def test_session_graphs_and_staged_match_eager(cuda, staged):
     assert len({int(o[0].float().sum()) for o in outs}) > 1, "inputs must change between steps"
 
 
+@pytest.mark.parametrize("tail_only", [False, True])
 @pytest.mark.parametrize("kv_dtype", ["int8", "fp8_e4m3"])
-def test_decode_step_matches_two_calls(cuda, kv_dtype):
+def test_decode_step_matches_two_calls(cuda, kv_dtype, tail_only):
     """kvq_decode_step (K2 PDL-launched behind K1) == quantize_append then
     paged_decode_attention: identical pages, identical output, eager and in a
     CUDA graph replayed with new rows; the appended rows are visible to K2."""
@@ -148,7 +149,8 @@ def test_decode_step_matches_two_calls(cuda, kv_dtype):
     k = torch.randn((sc.B, 8, 128), device=cuda, generator=g).to(torch.bfloat16)
     v = torch.randn((sc.B, 8, 128), device=cuda, generator=g).to(torch.bfloat16)
     q = torch.randn((sc.B, 32, 128), device=cuda, generator=g).to(torch.bfloat16)
-    out_a = decode_step(a, k, v, slots, q, table, lens1, out_dtype=torch.float32, pages_per_split=8)
+    out_a = decode_step(a, k, v, slots, q, table, lens1, out_dtype=torch.float32, pages_per_split=8,
+                        append_tail_only=tail_only)
     quantize_append(b, k, v, slots)
     out_b = paged_decode_attention(q, b, table, lens1, out_dtype=torch.float32, pages_per_split=8)
     torch.cuda.synchronize()
@@ -159,11 +161,11 @@ def test_decode_step_matches_two_calls(cuda, kv_dtype):
     out_g = torch.empty((sc.B, 32, 128), dtype=torch.float32, device=cuda)
     gr = torch.cuda.CUDAGraph()
     decode_step(a, k, v, slots, q, table, lens1, out=out_g, out_dtype=torch.float32, pages_per_split=8,
-                workspace=ws)
+                workspace=ws, append_tail_only=tail_only)
     torch.cuda.synchronize()
     with torch.cuda.graph(gr):
         decode_step(a, k, v, slots, q, table, lens1, out=out_g, out_dtype=torch.float32, pages_per_split=8,
-                    workspace=ws)
+                    workspace=ws, append_tail_only=tail_only)
     for _ in range(3):
         k.copy_(torch.randn((sc.B, 8, 128), device=cuda, generator=g).to(torch.bfloat16))
         v.copy_(torch.randn((sc.B, 8, 128), device=cuda, generator=g).to(torch.bfloat16))
@@ -254,3 +256,40 @@ def test_serving_loop_growing_sequences(cuda):
         assert torch.equal(a, b)
     assert torch.equal(ca.pool, cb.pool)
     alloc.check_invariants()
+
+
+@pytest.mark.parametrize("kv_dtype", ["int8", "fp8_e4m3"])
+def test_decode_step_tail_only_with_prefill_rows(cuda, kv_dtype):
+    """The C5 shape of a step: one append carries whole prefill chunks of
+    sequences K2 does not attend plus each attended sequence's newest token;
+    with append_tail_only the result equals the two calls in sequence."""
+    from paper_2605_29639_b200 import BlockAllocator
+    Hq, Hkv = 32, 8
+    alloc = BlockAllocator(600)
+    g = torch.Generator().manual_seed(4)
+    a = PagedKVCache(KVCacheSpec(Hkv, kv_dtype=kv_dtype), 600, device=cuda)
+    dec = list(range(12))
+    for s in dec:                                    # attended sequences with history
+        alloc.allocate(s)
+        sl = torch.tensor(alloc.append_slots(s, 37 * (s + 1)), dtype=torch.int32, device=cuda)
+        kv = torch.randn((2, sl.numel(), Hkv, 128), generator=g).to(torch.bfloat16).to(cuda)
+        quantize_append(a, kv[0], kv[1], sl)
+    b = PagedKVCache(KVCacheSpec(Hkv, kv_dtype=kv_dtype), 600, device=cuda, pool=a.pool.clone())
+    for p in ("p0", "p1"):                           # prefill chunks (not attended this step)
+        alloc.allocate(p)
+    pre = alloc.append_slots("p0", 2048) + alloc.append_slots("p1", 1000)
+    tail = alloc.append_one(dec).tolist()
+    slots = torch.tensor(pre + tail, dtype=torch.int32, device=cuda)
+    T = slots.numel()
+    k = torch.randn((T, Hkv, 128), generator=g).to(torch.bfloat16).to(cuda)
+    v = torch.randn((T, Hkv, 128), generator=g).to(torch.bfloat16).to(cuda)
+    q = torch.randn((len(dec), Hq, 128), generator=g).to(torch.bfloat16).to(cuda)
+    table = torch.from_numpy(alloc.block_table(dec)).to(cuda)
+    lens = torch.from_numpy(alloc.seq_lens(dec)).to(cuda)
+    out_a = decode_step(a, k, v, slots, q, table, lens, out_dtype=torch.float32, pages_per_split=4,
+                        append_tail_only=True)
+    quantize_append(b, k, v, slots)
+    out_b = paged_decode_attention(q, b, table, lens, out_dtype=torch.float32, pages_per_split=4)
+    torch.cuda.synchronize()
+    assert torch.equal(a.pool, b.pool)
+    assert torch.equal(out_a, out_b)

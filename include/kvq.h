@@ -40,7 +40,7 @@
 extern "C" {
 #endif
 
-#define KVQ_ABI_VERSION 1
+#define KVQ_ABI_VERSION 2 /* 2: peer gather, decode_step (+flags), pipeline submitter, block gather/scatter */
 #define KVQ_HEAD_DIM 128  /* d */
 #define KVQ_BLOCK_SIZE 16 /* tokens per page */
 #define KVQ_PAGE_BYTES 4224 /* one (block, kv head): 2x16x128 codes + 2x16 fp32 scales */

@@ -13,6 +13,7 @@ from pathlib import Path
 
 from ._build import LIB_PATH
 
+ABI_VERSION = 2  # include/kvq.h KVQ_ABI_VERSION
 KVQ_OK, KVQ_EINVAL, KVQ_EUNSUPPORTED, KVQ_ECUDA = 0, -1, -2, -3
 KVQ_INT8, KVQ_FP8_E4M3 = 0, 1
 KVQ_OUT_BF16, KVQ_OUT_F32 = 0, 1
@@ -98,8 +99,8 @@ def load(path: Path | str | None = None) -> ctypes.CDLL:
     for name, (res, args) in SIGNATURES.items():
         fn = getattr(lib, name)
         fn.restype, fn.argtypes = res, args
-    if lib.kvq_version() != 1:
-        raise ImportError(f"libkvq ABI version {lib.kvq_version()} != 1")
+    if lib.kvq_version() != ABI_VERSION:
+        raise ImportError(f"libkvq ABI version {lib.kvq_version()} != {ABI_VERSION} (stale build: rebuild it)")
     if path is None:
         _lib = lib
     return lib

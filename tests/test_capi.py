@@ -27,7 +27,7 @@ def test_library_exports_every_symbol():
     for name in declared_functions():
         assert hasattr(lib, name), name
     L = _lib.load()
-    assert L.kvq_version() == 1 and L.kvq_page_bytes() == 4224
+    assert L.kvq_version() == _lib.ABI_VERSION == 2 and L.kvq_page_bytes() == 4224
 
 
 def test_host_only_entry_points():

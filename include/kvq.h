@@ -193,6 +193,19 @@ int kvq_decode_step(const void* k, const void* v, int64_t k_token_stride, int64_
                     void* out, int32_t out_dtype, int32_t out_layout, const kvq_peer_out* peer,
                     int32_t flags, void* stream);
 
+/* Speculative-decoding verify step: kvq_decode_step with q_len
+ * new tokens per sequence -- K1 appends their rows, then the causal
+ * multi-query K2 of kvq_decode_attn_mq (q: bf16 [B][q_len][Hq][128]).  The
+ * tail-only flag is ignored for q_len > 1 (the new rows may span two pages);
+ * no fused gather (peer must be NULL unless q_len == 1). */
+int kvq_decode_step_mq(const void* k, const void* v, int64_t k_token_stride, int64_t v_token_stride,
+                       const int32_t* slot_mapping, int32_t T, const void* q, int64_t q_batch_stride,
+                       int32_t q_len, void* pool, int64_t num_blocks, const int32_t* block_table,
+                       int32_t max_blocks, const int32_t* seq_lens, int32_t B, int32_t Hq, int32_t Hkv,
+                       int32_t kv_dtype, float sm_scale, int32_t pages_per_split, void* workspace,
+                       size_t workspace_bytes, void* out, int32_t out_dtype, int32_t out_layout,
+                       const kvq_peer_out* peer, int32_t flags, void* stream);
+
 /* Host-side step submission of a double-buffered serving pipeline, in one
  * native call instead of ~10 runtime calls from the host language: upload the
  * step's packed inputs (pinned host -> device) on `h2d_stream`, run the slot's

@@ -47,6 +47,9 @@ SIGNATURES = {
     "kvq_decode_step": (_c.c_int, [_vp, _vp, _i64, _i64, _vp, _i32, _vp, _i64, _vp, _i64, _vp, _i32, _vp,
                                    _i32, _i32, _i32, _i32, _f32, _i32, _vp, _sz, _vp, _i32, _i32, _vp, _i32,
                                    _vp]),
+    "kvq_decode_step_mq": (_c.c_int, [_vp, _vp, _i64, _i64, _vp, _i32, _vp, _i64, _i32, _vp, _i64, _vp, _i32,
+                                      _vp, _i32, _i32, _i32, _i32, _f32, _i32, _vp, _sz, _vp, _i32, _i32, _vp,
+                                      _i32, _vp]),
     "kvq_pipeline_submit": (_c.c_int, [_vp]),
     "kvq_sym_alloc": (_c.c_int, [_sz, _c.POINTER(_vp), _vp]),
     "kvq_sym_open": (_c.c_int, [_vp, _c.POINTER(_vp)]),

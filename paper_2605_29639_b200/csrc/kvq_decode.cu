@@ -960,14 +960,16 @@ static int decode_attn_impl(const void* q, int64_t q_batch_stride, int32_t q_len
   return hi ? launch(kvq::decode_kernel<KVQ_FP8_E4M3, true, 0>) : launch(kvq::decode_kernel<KVQ_FP8_E4M3, false, 0>);
 }
 
-int kvq_decode_step(const void* k, const void* v, int64_t k_token_stride, int64_t v_token_stride,
-                    const int32_t* slot_mapping, int32_t T, const void* q, int64_t q_batch_stride,
-                    void* pool, int64_t num_blocks, const int32_t* block_table, int32_t max_blocks,
-                    const int32_t* seq_lens, int32_t B, int32_t Hq, int32_t Hkv, int32_t kv_dtype,
-                    float sm_scale, int32_t pages_per_split, void* workspace, size_t workspace_bytes,
-                    void* out, int32_t out_dtype, int32_t out_layout, const kvq_peer_out* peer,
-                    int32_t flags, void* stream) {
+int kvq_decode_step_mq(const void* k, const void* v, int64_t k_token_stride, int64_t v_token_stride,
+                       const int32_t* slot_mapping, int32_t T, const void* q, int64_t q_batch_stride,
+                       int32_t q_len, void* pool, int64_t num_blocks, const int32_t* block_table,
+                       int32_t max_blocks, const int32_t* seq_lens, int32_t B, int32_t Hq, int32_t Hkv,
+                       int32_t kv_dtype, float sm_scale, int32_t pages_per_split, void* workspace,
+                       size_t workspace_bytes, void* out, int32_t out_dtype, int32_t out_layout,
+                       const kvq_peer_out* peer, int32_t flags, void* stream) {
   if (flags & ~KVQ_STEP_APPEND_TAIL_ONLY) return fail(KVQ_EINVAL, "decode_step: unknown flags");
+  if (q_len <= 0) return fail(KVQ_EINVAL, "decode_step: bad q_len");
+  if (peer && q_len != 1) return fail(KVQ_EINVAL, "decode_step: the fused gather takes one query token per sequence");
   if (peer && (out_dtype != KVQ_OUT_BF16 || out_layout != KVQ_OUT_HBD))
     return fail(KVQ_EINVAL, "decode_step: the fused gather writes bf16 head-major rows");
   if (int rc = kvq_quant_append(k, v, k_token_stride, v_token_stride, slot_mapping, T, Hkv, kv_dtype, pool,
@@ -985,9 +987,24 @@ int kvq_decode_step(const void* k, const void* v, int64_t k_token_stride, int64_
   }
   // K2 is launched with programmatic stream serialization right behind K1, so
   // its launch and prologue overlap K1 (K1 never writes q, the table or lens).
-  return decode_attn_impl(q, q_batch_stride, 1, pool, num_blocks, block_table, max_blocks, seq_lens, B, Hq,
+  // q_len > 1 new tokens may span two pages: the tail-only wait does not apply.
+  const bool tail_only = (flags & KVQ_STEP_APPEND_TAIL_ONLY) != 0 && q_len == 1;
+  return decode_attn_impl(q, q_batch_stride, q_len, pool, num_blocks, block_table, max_blocks, seq_lens, B, Hq,
                           Hkv, kv_dtype, sm_scale, pages_per_split, workspace, workspace_bytes, out, out_dtype,
-                          out_layout, peer, stream, /*pdl=*/T > 0, (flags & KVQ_STEP_APPEND_TAIL_ONLY) != 0);
+                          out_layout, peer, stream, /*pdl=*/T > 0, tail_only);
+}
+
+int kvq_decode_step(const void* k, const void* v, int64_t k_token_stride, int64_t v_token_stride,
+                    const int32_t* slot_mapping, int32_t T, const void* q, int64_t q_batch_stride,
+                    void* pool, int64_t num_blocks, const int32_t* block_table, int32_t max_blocks,
+                    const int32_t* seq_lens, int32_t B, int32_t Hq, int32_t Hkv, int32_t kv_dtype,
+                    float sm_scale, int32_t pages_per_split, void* workspace, size_t workspace_bytes,
+                    void* out, int32_t out_dtype, int32_t out_layout, const kvq_peer_out* peer,
+                    int32_t flags, void* stream) {
+  return kvq_decode_step_mq(k, v, k_token_stride, v_token_stride, slot_mapping, T, q, q_batch_stride, 1, pool,
+                            num_blocks, block_table, max_blocks, seq_lens, B, Hq, Hkv, kv_dtype, sm_scale,
+                            pages_per_split, workspace, workspace_bytes, out, out_dtype, out_layout, peer, flags,
+                            stream);
 }
 
 int kvq_decode_attn_mq(const void* q, int64_t q_batch_stride, int32_t q_len, const void* pool,

@@ -232,14 +232,23 @@ def decode_step(cache: PagedKVCache, k: torch.Tensor, v: torch.Tensor, slot_mapp
     ``append_tail_only=True`` promises that, for every attended sequence, the
     appended rows lie in its last page (true of a decode step's new token;
     rows of sequences not in ``q``, e.g. prefill chunks, may go anywhere):
-    K2 then streams all other pages while K1 runs."""
+    K2 then streams all other pages while K1 runs.
+
+    ``q`` of shape ``[B, q_len, Hq, 128]`` makes it a speculative-decoding
+    verify step (``kvq_decode_step_mq``): the ``q_len`` draft tokens' rows are
+    appended and scored causally, as :func:`paged_decode_attention` does for a
+    4-D ``q`` (``append_tail_only`` does not apply; no ``peer``)."""
     _check_append("decode_step", cache, k, v, slot_mapping)
     _require_cuda("decode_step", q, block_table, seq_lens)
     spec = cache.spec
-    if q.dtype != torch.bfloat16 or q.dim() != 3 or q.shape[-1] != 128 or q.stride(-1) != 1 \
+    multi = q.dim() == 4
+    if q.dtype != torch.bfloat16 or q.dim() not in (3, 4) or q.shape[-1] != 128 or q.stride(-1) != 1 \
             or q.stride(-2) != 128:
-        raise ValueError("decode_step: q must be bf16 [B, Hq, 128] with contiguous heads")
-    B, Hq = q.shape[0], q.shape[1]
+        raise ValueError("decode_step: q must be bf16 [B, Hq, 128] or [B, q_len, Hq, 128], contiguous heads")
+    B, Hq = q.shape[0], q.shape[-2]
+    q_len = q.shape[1] if multi else 1
+    if multi and (q.stride(1) != Hq * 128 or peer is not None):
+        raise ValueError("decode_step: multi-query q needs contiguous tokens and no peer gather")
     if block_table.dtype != torch.int32 or block_table.dim() != 2 or block_table.shape[0] != B \
             or not block_table.is_contiguous():
         raise ValueError("decode_step: block_table must be contiguous int32 [B, max_blocks]")
@@ -253,7 +262,7 @@ def decode_step(cache: PagedKVCache, k: torch.Tensor, v: torch.Tensor, slot_mapp
         out, out_dtype, head_major = peer.out(slot), torch.bfloat16, True
         desc = ctypes.addressof(peer.descs[slot])
     else:
-        shape = (Hq, B, 128) if head_major else (B, Hq, 128)
+        shape = (Hq, B * q_len, 128) if head_major else ((B, q_len, Hq, 128) if multi else (B, Hq, 128))
         if out is None:
             out = torch.empty(shape, dtype=out_dtype, device=q.device)
         elif tuple(out.shape) != shape or out.dtype != out_dtype or not out.is_contiguous():
@@ -267,14 +276,15 @@ def decode_step(cache: PagedKVCache, k: torch.Tensor, v: torch.Tensor, slot_mapp
     pps = pages_per_split or lib.kvq_decode_pages_per_split(
         B, spec.num_kv_heads, total_pages if total_pages is not None else B * max_blocks, max_blocks)
     max_splits = -(-max_blocks // pps)
-    nbytes = lib.kvq_decode_workspace_bytes(B, Hq, spec.num_kv_heads, max_splits)
+    nbytes = lib.kvq_decode_workspace_bytes(B, Hq * q_len, spec.num_kv_heads, max_splits)
     if workspace is None:
         workspace = _workspace(q.device, nbytes, ((B * spec.num_kv_heads * 4 + 255) // 256) * 256)
     elif workspace.numel() * workspace.element_size() < nbytes:
         raise ValueError(f"decode_step: workspace needs {nbytes} bytes")
-    st = lib.kvq_decode_step(
+    st = lib.kvq_decode_step_mq(
         k.data_ptr(), v.data_ptr(), k.stride(0), v.stride(0), slot_mapping.data_ptr(), k.shape[0],
-        q.data_ptr(), q.stride(0), cache.pool.data_ptr(), cache.num_blocks, block_table.data_ptr(), max_blocks,
+        q.data_ptr(), q.stride(0), q_len, cache.pool.data_ptr(), cache.num_blocks, block_table.data_ptr(),
+        max_blocks,
         seq_lens.data_ptr(), B, Hq, spec.num_kv_heads, spec.kv_dtype_id, float(sm_scale), int(pps),
         workspace.data_ptr(), workspace.numel() * workspace.element_size(), out.data_ptr(),
         _lib.KVQ_OUT_F32 if out_dtype == torch.float32 else _lib.KVQ_OUT_BF16,

@@ -18,7 +18,7 @@ def declared_functions():
 
 def test_header_matches_binding():
     names = declared_functions()
-    assert len(names) == 19
+    assert len(names) == 20
     assert set(names) == set(_lib.SIGNATURES)
 
 

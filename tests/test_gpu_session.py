@@ -293,3 +293,38 @@ def test_decode_step_tail_only_with_prefill_rows(cuda, kv_dtype):
     torch.cuda.synchronize()
     assert torch.equal(a.pool, b.pool)
     assert torch.equal(out_a, out_b)
+
+
+@pytest.mark.parametrize("q_len", [2, 4])
+def test_decode_step_speculative_verify(cuda, q_len):
+    """decode_step with q [B, q_len, Hq, d] (kvq_decode_step_mq): appending
+    the q_len draft tokens' rows and scoring them causally equals
+    quantize_append then the multi-query paged_decode_attention."""
+    from paper_2605_29639_b200 import BlockAllocator
+    Hq, Hkv, B = 32, 8, 5
+    alloc = BlockAllocator(300)
+    g = torch.Generator().manual_seed(q_len)
+    a = PagedKVCache(KVCacheSpec(Hkv), 300, device=cuda)
+    for s, n in enumerate([15, 16, 33, 200, 1]):
+        alloc.allocate(s)
+        sl = torch.tensor(alloc.append_slots(s, n), dtype=torch.int32, device=cuda)
+        kv = torch.randn((2, n, Hkv, 128), generator=g).to(torch.bfloat16).to(cuda)
+        quantize_append(a, kv[0], kv[1], sl)
+    b = PagedKVCache(KVCacheSpec(Hkv), 300, device=cuda, pool=a.pool.clone())
+    slots = []
+    for s in range(B):                                  # q_len draft tokens per sequence, batch-major
+        slots += alloc.append_slots(s, q_len)
+    slots = torch.tensor(slots, dtype=torch.int32, device=cuda)
+    k = torch.randn((B * q_len, Hkv, 128), generator=g).to(torch.bfloat16).to(cuda)
+    v = torch.randn((B * q_len, Hkv, 128), generator=g).to(torch.bfloat16).to(cuda)
+    q = torch.randn((B, q_len, Hq, 128), generator=g).to(torch.bfloat16).to(cuda)
+    table = torch.from_numpy(alloc.block_table(list(range(B)))).to(cuda)
+    lens = torch.from_numpy(alloc.seq_lens(list(range(B)))).to(cuda)
+    out_a = decode_step(a, k, v, slots, q, table, lens, out_dtype=torch.float32, pages_per_split=4,
+                        append_tail_only=True)      # ignored for q_len > 1
+    quantize_append(b, k, v, slots)
+    out_b = paged_decode_attention(q, b, table, lens, out_dtype=torch.float32, pages_per_split=4)
+    torch.cuda.synchronize()
+    assert out_a.shape == (B, q_len, Hq, 128)
+    assert torch.equal(a.pool, b.pool)
+    assert torch.equal(out_a, out_b)

@@ -9,6 +9,7 @@
 #include <stdio.h>
 #include <string.h>
 
+#include <atomic>
 #include <type_traits>
 
 #include "kvq.h"
@@ -190,12 +191,15 @@ inline int check_launch(const char* what) {
   return KVQ_OK;
 }
 inline int check_device() {
+  static std::atomic<unsigned long long> verified{0};  // bit d: device d is sm_100 (checked once)
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return fail(KVQ_ECUDA, "cudaGetDevice failed");
+  if (dev < 64 && ((verified.load(std::memory_order_relaxed) >> dev) & 1ull)) return KVQ_OK;
   int major = 0, minor = 0;
   cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
   cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev);
   if (major != 10 || minor != 0) return fail(KVQ_EUNSUPPORTED, "libkvq is built for sm_100a (B200) only");
+  if (dev < 64) verified.fetch_or(1ull << dev, std::memory_order_relaxed);
   return KVQ_OK;
 }
 inline bool aligned(const void* p, size_t a) { return (reinterpret_cast<uintptr_t>(p) % a) == 0; }

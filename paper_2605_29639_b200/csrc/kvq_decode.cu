@@ -5,6 +5,10 @@
 // kvq_decode_attn{,_mq,_peer}, kvq_decode_step, split geometry, workspace.
 #include "kvq_common.cuh"
 
+#include <mutex>
+#include <set>
+#include <utility>
+
 namespace kvq {
 
 // ---------------------------------------------------------------------------
@@ -862,6 +866,24 @@ int32_t kvq_decode_pages_per_split(int32_t B, int32_t Hkv, int64_t total_pages, 
   return (int32_t)(pps > 0 ? pps : 1);
 }
 
+// Function attributes (dynamic smem size, max-shared carveout) are set once
+// per (device, kernel variant), not on every launch: two cudaFuncSetAttribute
+// calls cost microseconds of host time per call on the eager path.
+static cudaError_t set_attributes_once(const void* kernel, int smem_bytes) {
+  static std::mutex mu;
+  static std::set<std::pair<int, const void*>> done;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lock(mu);
+  if (done.count({dev, kernel})) return cudaSuccess;
+  e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
+  if (e == cudaSuccess) done.insert({dev, kernel});
+  return e;
+}
+
 static int decode_attn_impl(const void* q, int64_t q_batch_stride, int32_t q_len, const void* pool,
                             int64_t num_blocks, const int32_t* block_table, int32_t max_blocks,
                             const int32_t* seq_lens, int32_t B, int32_t Hq, int32_t Hkv, int32_t kv_dtype,
@@ -927,11 +949,7 @@ static int decode_attn_impl(const void* q, int64_t q_batch_stride, int32_t q_len
   const bool hi = prm.G > 8;
   const size_t smem_bytes = hi ? kvq::Geo<true>::SMEM : kvq::Geo<false>::SMEM;
   auto launch = [&](auto kernel) -> int {
-    cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)smem_bytes);
-    if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
-                               cudaSharedmemCarveoutMaxShared);
+    cudaError_t e = set_attributes_once(reinterpret_cast<const void*>(kernel), (int)smem_bytes);
     if (e != cudaSuccess) return fail(KVQ_ECUDA, cudaGetErrorString(e));
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = grid;

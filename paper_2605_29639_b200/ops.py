@@ -24,7 +24,11 @@ _WS_CACHE: Dict[Tuple[int, int], list] = {}
 
 
 def _stream_handle(device: torch.device) -> int:
-    return torch.cuda.current_stream(device).cuda_stream
+    """Raw cudaStream_t of the current stream (torch's C accessor when present:
+    ``torch.cuda.current_stream()`` costs several microseconds per call)."""
+    idx = device.index if device.index is not None else torch.cuda.current_device()
+    raw = getattr(torch._C, "_cuda_getCurrentRawStream", None)
+    return raw(idx) if raw is not None else torch.cuda.current_stream(device).cuda_stream
 
 
 def _require_cuda(name: str, *ts: torch.Tensor) -> None:

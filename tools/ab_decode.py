@@ -14,7 +14,7 @@ import sys
 import numpy as np
 import torch
 
-SHAPES = {"c2f": (256, 32, 8, "ragged", 1), "c3i": (128, 64, 8, 32768, 0), "c2e": (256, 32, 8, 4352, 0), "c1": (8, 32, 8, 2048, 0), "c2": (256, 32, 8, "ragged", 0), "c3": (128, 64, 8, 32768, 1), "c4": (64, 64, 4, 131072, 0)}
+SHAPES = {"tiny": (1, 32, 8, 15, 0), "b1_2k": (1, 32, 8, 2048, 0), "b8_512": (8, 32, 8, 512, 0), "c2f": (256, 32, 8, "ragged", 1), "c3i": (128, 64, 8, 32768, 0), "c2e": (256, 32, 8, 4352, 0), "c1": (8, 32, 8, 2048, 0), "c2": (256, 32, 8, "ragged", 0), "c3": (128, 64, 8, 32768, 1), "c4": (64, 64, 4, 131072, 0)}
 
 
 def main():
@@ -51,7 +51,8 @@ def main():
         vp, i32, i64 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64
         L.kvq_decode_attn.argtypes = [vp, i64, vp, i64, vp, i32, vp, i32, i32, i32, i32, ctypes.c_float, i32,
                                       vp, ctypes.c_size_t, vp, i32, i32, vp]
-        pps = L.kvq_decode_pages_per_split(B, Hkv, NB, mb)
+        import os
+        pps = int(os.environ.get("PPS", 0)) or L.kvq_decode_pages_per_split(B, Hkv, NB, mb)
         wsb = L.kvq_decode_workspace_bytes(B, Hq, Hkv, -(-mb // pps))
         ws = torch.zeros(wsb, dtype=torch.uint8, device=dev)
 
@@ -77,7 +78,7 @@ def main():
     byt = int(lens.sum()) * Hkv * 264 + B * Hq * 512 + int(nblk.sum()) * 4
     for path, _, times in runs:
         t = min(times)
-        print(f"{cfg} {path}: min {t * 1e3:.1f} us  median {sorted(times)[2] * 1e3:.1f} us  "
+        print(f"{cfg} pps={pps} {path}: min {t * 1e3:.1f} us  median {sorted(times)[2] * 1e3:.1f} us  "
               f"{byt / t / 1e6:.0f} GB/s")
 
 

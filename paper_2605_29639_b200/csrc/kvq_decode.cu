@@ -5,6 +5,8 @@
 // kvq_decode_attn{,_mq,_peer}, kvq_decode_step, split geometry, workspace.
 #include "kvq_common.cuh"
 
+#include <algorithm>
+
 #include <mutex>
 #include <set>
 #include <utility>
@@ -839,8 +841,9 @@ size_t kvq_decode_workspace_bytes(int32_t B, int32_t Hq, int32_t Hkv, int32_t ma
 }
 
 int32_t kvq_decode_pages_per_split(int32_t B, int32_t Hkv, int64_t total_pages, int32_t max_blocks) {
-  // Uniform splits of <= 128 pages (540 KB of KV per CTA) so the ragged tail is
-  // at most one short CTA; as few waves of CTAs_PER_SM x SMs as that allows.
+  // Large launches: uniform splits of <= 128 pages (540 KB of KV per CTA) so the
+  // ragged tail is at most one short CTA (512 for equal lengths); as few waves
+  // of CTAs_PER_SM x SMs as that allows.  Small launches: a latency cost model.
   int sms = 148, dev = 0;
   if (cudaGetDevice(&dev) == cudaSuccess) {
     int v = 0;
@@ -850,6 +853,34 @@ int32_t kvq_decode_pages_per_split(int32_t B, int32_t Hkv, int64_t total_pages, 
   }
   const int64_t slots = (int64_t)sms * kvq::CTAS_PER_SM;
   const int64_t work = total_pages * (int64_t)Hkv;
+  if (max_blocks > 0 && work <= slots * 128) {
+    // Small, latency-bound launch (one wave at 128-page splits): pick the split
+    // size from a cost model fitted to CUDA-graph timings of B = 1..32 shapes
+    // (tools/ab_decode.py GRAPH=1 PPS=...):
+    //   t = waves * (4.5 us + pages_per_cta * t_page) + 0.14 us * (splits - 1),
+    //   t_page = max(concurrent CTAs * 4224 B / 6.9 TB/s, 0.22 us),
+    // the last term being the fused combine (one CTA merges every split).
+    static const int cand[] = {8, 9, 10, 12, 14, 16, 19, 22, 26, 30, 35, 41, 48, 56, 64, 75, 88, 103, 120, 140,
+                               164, 192, 224, 262, 306, 358, 419, 490, 573, 670, 784, 917, 1073, 1255};
+    const int64_t per = max_blocks;  // the longest sequence sets the latency
+    const int64_t pairs0 = (int64_t)B * Hkv;
+    double best_t = 1e30;
+    int64_t best = per < 8 ? per : 8;
+    for (int c : cand) {
+      if (c > per) break;
+      const int64_t ns = (per + c - 1) / c;
+      const int64_t pps_eff = (per + ns - 1) / ns;
+      const int64_t ctas = pairs0 * ns;
+      const int64_t nw = (ctas + slots - 1) / slots;
+      const double tpage = std::max((double)std::min(ctas, slots) * 4224.0 / 6.9e6, 0.22);
+      const double t = nw * (4.5 + pps_eff * tpage) + 0.14 * (ns - 1);
+      if (t < best_t) {
+        best_t = t;
+        best = pps_eff;
+      }
+    }
+    return (int32_t)std::max<int64_t>(1, std::min<int64_t>(best, per));
+  }
   // Equal-length batches have no ragged tail to protect: allow 512-page
   // splits (4x less split prologue / partial traffic / combine work).
   const bool uniform = max_blocks > 0 && total_pages * 20 >= (int64_t)B * max_blocks * 19;

@@ -6,7 +6,9 @@ exports kvq_decode_attn / kvq_decode_pages_per_split / workspace_bytes).
 CONFIG is one of c2, c3, c4 (bench.py shapes).  Pages are random codes with
 fixed positive scales (timing only); block ids are a random permutation.
 Each lib is timed in alternation (5 rounds x 20 launches, CUDA events), so
-box-level drift affects every build alike.
+box-level drift affects every build alike.  GRAPH=1 replays the 20 launches
+from one CUDA graph (GPU time without host launch cost); PPS=n forces the
+split size.
 """
 import ctypes
 import sys
@@ -14,7 +16,7 @@ import sys
 import numpy as np
 import torch
 
-SHAPES = {"tiny": (1, 32, 8, 15, 0), "b1_2k": (1, 32, 8, 2048, 0), "b8_512": (8, 32, 8, 512, 0), "c2f": (256, 32, 8, "ragged", 1), "c3i": (128, 64, 8, 32768, 0), "c2e": (256, 32, 8, 4352, 0), "c1": (8, 32, 8, 2048, 0), "c2": (256, 32, 8, "ragged", 0), "c3": (128, 64, 8, 32768, 1), "c4": (64, 64, 4, 131072, 0)}
+SHAPES = {"b1_32k": (1, 32, 8, 32768, 0), "b4_8k": (4, 32, 8, 8192, 0), "b32_2k": (32, 32, 8, 2048, 0), "tiny": (1, 32, 8, 15, 0), "b1_2k": (1, 32, 8, 2048, 0), "b8_512": (8, 32, 8, 512, 0), "c2f": (256, 32, 8, "ragged", 1), "c3i": (128, 64, 8, 32768, 0), "c2e": (256, 32, 8, 4352, 0), "c1": (8, 32, 8, 2048, 0), "c2": (256, 32, 8, "ragged", 0), "c3": (128, 64, 8, 32768, 1), "c4": (64, 64, 4, 131072, 0)}
 
 
 def main():
@@ -59,22 +61,33 @@ def main():
         def launch(L=L, pps=pps, ws=ws, wsb=wsb):
             st = L.kvq_decode_attn(q.data_ptr(), q.stride(0), pool.data_ptr(), NB, table.data_ptr(), mb,
                                    seq.data_ptr(), B, Hq, Hkv, kvd, 0.0884, pps, ws.data_ptr(), wsb,
-                                   out.data_ptr(), 0, 1, stream)
+                                   out.data_ptr(), 0, 1, torch.cuda.current_stream().cuda_stream)
             assert st == 0, st
         launch()
         runs.append((path, launch, []))
     torch.cuda.synchronize()
+    import os
+    if os.environ.get("GRAPH"):  # time 20 launches captured in one CUDA graph: GPU time, no host cost
+        graphed = []
+        for path, launch, times in runs:
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                for _ in range(20):
+                    launch()
+            graphed.append((path, (lambda g=g: g.replay()), times))
+        runs = graphed
     for _ in range(5):
         for path, launch, times in runs:
+            reps = 1 if os.environ.get("GRAPH") else 20
             for _ in range(3):
                 launch()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
-            for _ in range(20):
+            for _ in range(reps):
                 launch()
             e1.record()
             torch.cuda.synchronize()
-            times.append(e0.elapsed_time(e1) / 20)
+            times.append(e0.elapsed_time(e1) / 20)  # 20 launches either way
     byt = int(lens.sum()) * Hkv * 264 + B * Hq * 512 + int(nblk.sum()) * 4
     for path, _, times in runs:
         t = min(times)

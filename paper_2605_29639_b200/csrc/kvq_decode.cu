@@ -788,6 +788,69 @@ __device__ __forceinline__ void decode_cta(const DecodeParams& p, uint8_t* smem)
   __syncthreads();
   if (!*flag) return;
   if constexpr (PEER) peer_acquire(p.peer);
+  if (!HI && nsplit >= 8 && G * nsplit + 16 <= NW * S * PAGE / 4) {
+    // Many splits (small batches over long contexts), g <= 8.  With 16 rows the
+    // per-item pairing below measured slower on C4, whose equal-length splits
+    // put a combine at every wave boundary; with a few splits the extra phase
+    // does not pay (A/B: tools/ab_decode.py GRAPH=1).
+    // Phase A: per row, the max LSE and normalised weights, once, into shared
+    // memory (the ring is free: every page was consumed).  Warps take rows,
+    // lanes take splits.
+    float* wsm = reinterpret_cast<float*>(smem);  // [G][nsplit] weights, then [G] 1 / sum
+    for (int row = warp; row < G; row += NW) {
+      const float* lse = p.part_lse + (((int64_t)b * p.Hkv + h) * G + row) * p.max_splits;
+      float M = -INFINITY;
+      for (int sp = lane; sp < nsplit; sp += 32) M = fmaxf(M, __ldcg(lse + sp));
+#pragma unroll
+      for (int o2 = 16; o2 > 0; o2 >>= 1) M = fmaxf(M, __shfl_xor_sync(FULL, M, o2));
+      float ws = 0.0f;
+      for (int sp = lane; sp < nsplit; sp += 32) {
+        const float w = fast_exp2(__ldcg(lse + sp) - M);
+        wsm[row * nsplit + sp] = w;
+        ws += w;
+      }
+#pragma unroll
+      for (int o2 = 16; o2 > 0; o2 >>= 1) ws += __shfl_xor_sync(FULL, ws, o2);
+      if (lane == 0) wsm[G * nsplit + row] = 1.0f / ws;
+    }
+    __syncthreads();
+    // Phase B: an item (row, 8 contiguous d) is shared by two neighbouring lanes,
+    // each summing half of the splits; one shuffle merges them.  G * 32 work
+    // units keep every thread's loads independent and in flight.
+    const int h1 = (nsplit + 1) >> 1;
+    for (int it = tid; it < nrow_items * 2; it += THREADS) {
+      const int item = it >> 1, half = it & 1;
+      const int row = item / (HD / 8), d0 = (item % (HD / 8)) * 8;
+      const int64_t base = (((int64_t)b * p.Hkv + h) * G + row) * p.max_splits;
+      const float* w = wsm + row * nsplit;
+      float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+      const int s0 = half ? h1 : 0, s1 = half ? nsplit : h1;
+#pragma unroll 4
+      for (int sp = s0; sp < s1; ++sp) {
+        const float wgt = w[sp];
+        const float4 a = __ldcg(reinterpret_cast<const float4*>(p.part_o + (base + sp) * HD + d0));
+        const float4 cc = __ldcg(reinterpret_cast<const float4*>(p.part_o + (base + sp) * HD + d0 + 4));
+        acc[0] += wgt * a.x;
+        acc[1] += wgt * a.y;
+        acc[2] += wgt * a.z;
+        acc[3] += wgt * a.w;
+        acc[4] += wgt * cc.x;
+        acc[5] += wgt * cc.y;
+        acc[6] += wgt * cc.z;
+        acc[7] += wgt * cc.w;
+      }
+#pragma unroll
+      for (int e = 0; e < 8; ++e) acc[e] += __shfl_xor_sync(FULL, acc[e], 1);
+      if (!half) {
+        const float inv = wsm[G * nsplit + row];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) acc[e] *= inv;
+        store_out<PEER>(p, b, h, row, d0, acc);
+      }
+    }
+    if constexpr (PEER) peer_signal(p.peer);
+    return;
+  }
   for (int item = tid; item < nrow_items; item += THREADS) {
     const int row = item / (HD / 8), d0 = (item % (HD / 8)) * 8;
     const int64_t base = (((int64_t)b * p.Hkv + h) * G + row) * p.max_splits;

@@ -946,7 +946,11 @@ int32_t kvq_decode_pages_per_split(int32_t B, int32_t Hkv, int64_t total_pages, 
   }
   // Equal-length batches have no ragged tail to protect: allow 512-page
   // splits (4x less split prologue / partial traffic / combine work).
-  const bool uniform = max_blocks > 0 && total_pages * 20 >= (int64_t)B * max_blocks * 19;
+  // (Only for big launches -- >= 8 waves at 128-page splits, e.g. C3 / C4: in the
+  // few-wave range the 512 cap left ~1 wave of very long CTAs, B = 32 x 8K
+  // 110 us vs 92 us at 128 pages.)
+  const bool uniform = max_blocks > 0 && total_pages * 20 >= (int64_t)B * max_blocks * 19 &&
+                       work >= slots * 128 * 8;
   const int64_t cap = uniform ? 512 : 128;
   const int64_t waves = (work + slots * cap - 1) / (slots * cap);
   int64_t pps = (work + slots * (waves > 0 ? waves : 1) - 1) / (slots * (waves > 0 ? waves : 1));

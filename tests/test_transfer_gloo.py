@@ -6,7 +6,6 @@ import os
 import socket
 
 import numpy as np
-import pytest
 import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
@@ -26,7 +25,6 @@ def _worker(rank, port, q):
     import oracle as O
     from kvq_testutil import bf16_bits, make_kv
     from paper_2605_29639_b200 import BlockAllocator, KVCacheSpec, PagedKVCache
-    from paper_2605_29639_b200.cache import unpack_pages
     from paper_2605_29639_b200.transfer import recv_sequence, send_sequence, wire_bytes_per_token
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=2)

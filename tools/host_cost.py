@@ -1,8 +1,8 @@
 """Host cost of an eager op call (a 1-page decode: the GPU work is negligible, so
 the loop is host-bound), plus a cProfile breakdown of the Python wrapper."""
-import sys, time, torch, numpy as np
+import sys, time, torch
 sys.path.insert(0, '.')
-from paper_2605_29639_b200 import KVCacheSpec, PagedKVCache, paged_decode_attention, decode_step
+from paper_2605_29639_b200 import KVCacheSpec, PagedKVCache, paged_decode_attention
 dev = torch.device('cuda:0')
 cache = PagedKVCache(KVCacheSpec(8), 64, device=dev)
 cache.pool[..., 4096:] = 0

@@ -45,14 +45,8 @@ constexpr int THREADS = 32 * NW;
 template <bool HI>
 struct Geo {
   static constexpr int NT = HI ? 2 : 1;
-#ifndef KVQ_HI_S
-#define KVQ_HI_S 3
-#endif
-#ifndef KVQ_HI_CTAS
-#define KVQ_HI_CTAS 4
-#endif
-  static constexpr int S = HI ? KVQ_HI_S : 3;          // ring slots (pages in flight) per warp
-  static constexpr int CTAS = HI ? KVQ_HI_CTAS : 4;    // resident CTAs per SM (regs + smem)
+  static constexpr int S = 3;     // ring slots (pages in flight) per warp
+  static constexpr int CTAS = 4;  // resident CTAs per SM (regs + smem)
   // g > 8 keeps the Q^T fragments in shared memory (one copy per CTA, read with
   // one conflict-free LDS.64 per k-step) so the live set fits 128 registers.
   static constexpr size_t QSM = HI ? (size_t)NT * 8 * 32 * 8 : 0;  // [nt][k-step pair][lane] uint4

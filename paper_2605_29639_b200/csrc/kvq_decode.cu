@@ -919,16 +919,22 @@ int32_t kvq_decode_pages_per_split(int32_t B, int32_t Hkv, int64_t total_pages, 
     // the last term being the fused combine (one CTA merges every split).
     static const int cand[] = {8, 9, 10, 12, 14, 16, 19, 22, 26, 30, 35, 41, 48, 56, 64, 75, 88, 103, 120, 140,
                                164, 192, 224, 262, 306, 358, 419, 490, 573, 670, 784, 917, 1073, 1255};
+    // Ragged batches (total below B * max_blocks): sum_b ceil(n_b / pps) is
+    // estimated as total / pps + B / 2 per head, and the waves count
+    // fractionally -- CTAs of unequal length backfill the slots a wave leaves.
+    // (C2's shape split over 8 ranks, one kv head each: 66 -> 55 us.)
     const int64_t per = max_blocks;  // the longest sequence sets the latency
     const int64_t pairs0 = (int64_t)B * Hkv;
+    const bool ragged = total_pages * 20 < (int64_t)B * max_blocks * 19;
     double best_t = 1e30;
     int64_t best = per < 8 ? per : 8;
     for (int c : cand) {
       if (c > per) break;
       const int64_t ns = (per + c - 1) / c;
       const int64_t pps_eff = (per + ns - 1) / ns;
-      const int64_t ctas = pairs0 * ns;
-      const int64_t nw = (ctas + slots - 1) / slots;
+      int64_t ctas = pairs0 * ns;
+      if (ragged) ctas = std::min(ctas, (int64_t)Hkv * ((total_pages + pps_eff - 1) / pps_eff + (B + 1) / 2));
+      const double nw = ragged ? std::max(1.0, (double)ctas / slots) : (double)((ctas + slots - 1) / slots);
       const double tpage = std::max((double)std::min(ctas, slots) * 4224.0 / 6.9e6, 0.22);
       const double t = nw * (4.5 + pps_eff * tpage) + 0.14 * (ns - 1);
       if (t < best_t) {

@@ -346,12 +346,20 @@ __device__ __forceinline__ void decode_cta(const DecodeParams& p, uint8_t* smem)
     for (int o = 16; o > 0; o >>= 1) amax = fmaxf(amax, __shfl_xor_sync(FULL, amax, o));
     if constexpr (KVD == KVQ_INT8) {
       // INT8 K feeds the s8 tensor cores directly (no dequantisation at all):
-      // q = s1 * (q1 + q2 / 128) with int8 q1, q2 (error <= amax / 32512), two
-      // IMMA per k-step, S = s1 * (acc1 + acc2 / 128).  IMMA k-step j (32 of d):
-      // b0 = q[head][16c + 4j .. +3], b1 = q[head][64 + 16c + 4j .. +3], stored as
-      // qf[nt][2j] = term 1 (b0, b1), qf[nt][2j + 1] = term 2.
-      const float s1 = amax / 127.0f;
-      const float inv1 = amax > 0.0f ? 127.0f / amax : 0.0f;
+      // q = s1 * (q1 + q2 / 128) with int8 q1, q2, two IMMA per k-step,
+      // S = s1 * (acc1 + acc2 / 128).  s1 is a power of two (amax / s1 in
+      // [64, 127.5), else one binade up), so the two terms hold every bf16
+      // element >= s1 (its 8-bit mantissa) EXACTLY; only elements below s1 ~
+      // amax / 100 round, by <= s1 / 256.  (With s1 = amax / 127 every element
+      // rounded: 2.3e-3 output error at logits of std 15, against 4.6e-4 now.)
+      // IMMA k-step j (32 of d): b0 = q[head][16c + 4j .. +3], b1 =
+      // q[head][64 + 16c + 4j .. +3], stored as qf[nt][2j] = term 1 (b0, b1),
+      // qf[nt][2j + 1] = term 2.
+      int qex = 0;
+      if (amax > 0.0f) frexpf(amax, &qex);  // amax = m * 2^qex, m in [0.5, 1)
+      if (amax * pow2i(7 - qex) > 127.49f) ++qex;
+      const float s1 = amax > 0.0f ? pow2i(qex - 7) : 0.0f;
+      const float inv1 = amax > 0.0f ? pow2i(7 - qex) : 0.0f;
       qscale = p.sm_scale_log2 * s1 * 0.0078125f;  // S = s1 * (128 acc1 + acc2) / 128
 #pragma unroll
       for (int nt = 0; nt < NT; ++nt)
@@ -623,9 +631,14 @@ __device__ __forceinline__ void decode_cta(const DecodeParams& p, uint8_t* smem)
             o[nt][mt][2] *= f[0];
             o[nt][mt][3] *= f[1];
           }
+          // Recompute from the ROUNDED product, as m was: the row's max token gets
+          // u = 0 exactly (p = 1, so l >= 1).  The fast path's FFMA is exact
+          // instead; the two differ by half an ulp of m, which only matters past
+          // |m| ~ 2^27 (log2 units; fp32 cannot resolve such scores) -- there the
+          // clamp keeps p <= 2^8 and the max token keeps l > 0 (no 0/0, no inf).
 #pragma unroll
           for (int q4 = 0; q4 < 4; ++q4) {
-            u[nt][q4] = fmaf(st[nt][q4], q4 < 2 ? kq_r : kq_r8, -m[nt][q4 & 1]);
+            u[nt][q4] = fminf(__fadd_rn(__fmul_rn(st[nt][q4], q4 < 2 ? kq_r : kq_r8), -m[nt][q4 & 1]), 8.0f);
             if (TAIL && !visible(nt, q4)) u[nt][q4] = -INFINITY;
           }
         }

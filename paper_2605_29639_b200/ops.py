@@ -79,10 +79,12 @@ def workspace_bytes(batch: int, num_q_heads: int, num_kv_heads: int, max_splits:
 
 def _workspace(device: torch.device, nbytes: int, counter_bytes: int) -> torch.Tensor:
     """Per-(device, stream) cached workspace.  Its first ``counter_bytes`` (the
-    split-combine arrival counters, offset 0) must be zero on entry; the kernel
-    leaves them zero, but a later call with a larger batch x kv-head count
-    moves the counter region over former partials, so that prefix is re-zeroed
-    whenever it grows."""
+    split-combine arrival counters, offset 0) must be zero on entry.  The
+    kernel leaves its own counters zero, but writes partials right after them,
+    so only the LAST call's counter region is known clean: a call with a
+    larger batch x kv-head count than the last one re-zeroes its prefix (a
+    large -> small -> large sequence would otherwise find the small call's
+    partials in its counters)."""
     key = (device.index if device.index is not None else torch.cuda.current_device(),
            _stream_handle(device))
     ent = _WS_CACHE.get(key)
@@ -91,7 +93,7 @@ def _workspace(device: torch.device, nbytes: int, counter_bytes: int) -> torch.T
         _WS_CACHE[key] = ent
     elif counter_bytes > ent[1]:
         ent[0][:counter_bytes].zero_()
-        ent[1] = counter_bytes
+    ent[1] = counter_bytes
     return ent[0]
 
 
@@ -115,7 +117,12 @@ def paged_decode_attention(q: torch.Tensor, cache: PagedKVCache, block_table: to
     ``out_dtype`` (bf16 or fp32).  ``total_pages`` (sum of per-sequence
     pages, when the host knows it) sharpens the split-KV geometry;
     ``num_splits`` (SURVEY §8b's name) instead fixes the split count of the
-    longest sequence: ``pages_per_split = ceil(max_blocks / num_splits)``."""
+    longest sequence: ``pages_per_split = ceil(max_blocks / num_splits)``.
+    ``workspace`` (uint8, ``workspace_bytes(...)`` long, zeroed before first
+    use; the kernel leaves it reusable for the same batch x kv-head count)
+    defaults to a per-stream cached buffer -- pass your own when capturing
+    the call in a CUDA graph, so eager calls of other shapes on the stream
+    cannot dirty the graph's split-combine counters."""
     _require_cuda("paged_decode_attention", q, block_table, seq_lens, cache.pool)
     spec = cache.spec
     multi = q.dim() == 4  # [B, q_len, Hq, 128]: speculative scoring / MTP (causal among the new tokens)

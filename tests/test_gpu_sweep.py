@@ -1,0 +1,114 @@
+"""Randomised K2 parity sweep against the CPU oracle: seeded random shapes
+(GQA group 1..16, 1..8 kv heads, ragged lengths with empty / one-token /
+page-boundary sequences), both code formats, automatic or random split
+geometry -- plus adversarial data (peaked softmax from large logits,
+all-zero and very large K/V rows).  Same tolerance as test_gpu_attention:
+per (sequence, head) row, max |err| <= 2e-3 * max |ref row|."""
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+from kvq_testutil import Scenario, bf16_bits
+from paper_2605_29639_b200 import KVCacheSpec, PagedKVCache, paged_decode_attention
+
+pytestmark = pytest.mark.gpu
+NAMES = {O.INT8: "int8", O.FP8_E4M3: "fp8_e4m3"}
+
+
+def rel_err(out, ref):
+    err = np.abs(out - ref).max(axis=-1)
+    scale = np.abs(ref).max(axis=-1)
+    return float((err / (scale + 1e-6 / 2e-3)).max())
+
+
+def run(sc, cuda, **kw):
+    cache = PagedKVCache(KVCacheSpec(sc.Hkv, kv_dtype=NAMES[sc.kv_dtype]), sc.num_blocks, device=cuda,
+                         pool=torch.from_numpy(sc.pool).to(cuda))
+    out = paged_decode_attention(sc.q.to(cuda), cache, torch.from_numpy(sc.block_table).to(cuda),
+                                 torch.from_numpy(sc.seq_lens).to(cuda), out_dtype=torch.float32, **kw)
+    return out.cpu().numpy()
+
+
+def random_case(seed):
+    rng = np.random.default_rng(1000 + seed)
+    Hkv = int(rng.choice([1, 2, 4, 8]))
+    g = int(rng.choice([1, 2, 4, 8, 16]))
+    B = int(rng.integers(1, 13))
+    special = [0, 1, 15, 16, 17, 32, 33]
+    lens = [int(rng.choice(special)) if rng.random() < 0.3 else int(rng.integers(1, 3000)) for _ in range(B)]
+    if max(lens) == 0:
+        lens[0] = 5
+    kvd = O.INT8 if rng.random() < 0.5 else O.FP8_E4M3
+    pps = None if rng.random() < 0.5 else int(rng.integers(1, 65))
+    return lens, g * Hkv, Hkv, kvd, pps
+
+
+@pytest.mark.parametrize("seed", range(24))
+def test_random_shapes(cuda, seed):
+    lens, Hq, Hkv, kvd, pps = random_case(seed)
+    sc = Scenario(lens, Hq, Hkv, kvd, seed=seed)
+    out = run(sc, cuda, pages_per_split=pps)
+    ref = sc.oracle_out()
+    assert np.isfinite(out).all()
+    for b, L in enumerate(lens):
+        if L == 0:
+            assert np.all(out[b] == 0)
+    assert rel_err(out, ref) <= 2e-3, (lens, Hq, Hkv, kvd, pps, rel_err(out, ref))
+
+
+def requantize(sc):
+    sc.pool[:] = 0
+    O.quant_append(bf16_bits(sc.k), bf16_bits(sc.v), sc.slots, sc.kv_dtype, sc.pool)
+
+
+@pytest.mark.parametrize("kv_dtype", [O.INT8, O.FP8_E4M3])
+@pytest.mark.parametrize("q_gain", [8.0, 40.0])
+def test_peaked_softmax_and_extreme_rows(cuda, kv_dtype, q_gain):
+    """Large logits make the running max jump mid-sequence (the lazy rescale
+    and the P exponent shift); zero rows have scale 0 and all-zero codes;
+    K rows of magnitude 2^100 give scores past fp32 resolution (the output
+    must stay finite and the max token must win); V rows 2^6 larger or
+    2^100 smaller than their page neighbours stress the per-page P' exponent
+    (P' is f16 with the page's largest V scale normalised, so
+    a dominant token whose V scale is below ~2^-8 of its page's largest
+    loses precision -- real KV stays within ~2^6 per page)."""
+    sc = Scenario([1800, 700, 64, 2500], 32, 8, kv_dtype, seed=77)
+    T = sc.k.shape[0]
+    g = torch.Generator().manual_seed(5)
+    idx = torch.randperm(T, generator=g)
+    k, v = sc.k.float(), sc.v.float()
+    k[idx[:40]] = 0.0
+    v[idx[40:80]] = 0.0
+    k[idx[80:100]] *= 2.0 ** 100
+    v[idx[100:120]] *= 2.0 ** 6
+    if q_gain <= 8.0:
+        # At 40x one token takes nearly all the weight; if its V is ~0 the
+        # output is made only of weights p < 2^-18, below f16's normal range
+        # for P' -- a property of 16-bit P, not a bug.
+        v[idx[120:140]] *= 2.0 ** -100
+    sc.k, sc.v = k.to(torch.bfloat16), v.to(torch.bfloat16)
+    requantize(sc)
+    sc.q = (sc.q.float() * q_gain).to(torch.bfloat16)
+    ref = sc.oracle_out()
+    for pps in (None, 3):
+        out = run(sc, cuda, pages_per_split=pps)
+        assert np.isfinite(out).all()
+        assert rel_err(out, ref) <= 2e-3, (pps, rel_err(out, ref))
+
+
+def test_cached_workspace_across_shapes(cuda):
+    """The per-stream cached workspace must stay correct when the batch x
+    kv-head count goes large -> small -> large (the small call's partials
+    land where the large call's split-combine counters live)."""
+    # 16 x 8 (b, kv head) counters = 512 B vs 2 x 4 -> 256 B: the small call's
+    # partials start inside the big call's counter region.
+    big = Scenario([900, 1700, 33, 2500, 1200, 64, 800, 1500] * 2, 32, 8, O.INT8, seed=90)
+    small = Scenario([3000, 2000], 32, 4, O.INT8, seed=91)
+    ref_big, ref_small = big.oracle_out(), small.oracle_out()
+    for _ in range(3):
+        for sc, ref, pps in ((big, ref_big, 4), (small, ref_small, 3)):
+            # fresh NaN output each call: a skipped combine must not pass on a
+            # previous call's result left in recycled memory
+            out = torch.full((sc.B, sc.Hq, 128), float("nan"), device=cuda)
+            assert rel_err(run(sc, cuda, pages_per_split=pps, out=out), ref) <= 2e-3

@@ -112,3 +112,45 @@ def test_cached_workspace_across_shapes(cuda):
             # previous call's result left in recycled memory
             out = torch.full((sc.B, sc.Hq, 128), float("nan"), device=cuda)
             assert rel_err(run(sc, cuda, pages_per_split=pps, out=out), ref) <= 2e-3
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_random_decode_steps(cuda, seed):
+    """decode_step (K1 + PDL-launched K2 in one call) on random shapes: the new
+    row of every sequence (opening a fresh block when its last page is full)
+    lands bit-exact where the oracle puts it, and the attention over the
+    grown sequences matches the oracle."""
+    from paper_2605_29639_b200 import decode_step
+    rng = np.random.default_rng(2000 + seed)
+    Hkv = int(rng.choice([1, 2, 4, 8]))
+    Hq = Hkv * int(rng.choice([1, 2, 4, 8, 16]))
+    B = int(rng.integers(1, 10))
+    lens = [int(rng.choice([0, 1, 15, 16, 32])) if rng.random() < 0.3 else int(rng.integers(1, 2500))
+            for _ in range(B)]
+    kvd = O.INT8 if seed % 2 == 0 else O.FP8_E4M3
+    sc = Scenario(lens, Hq, Hkv, kvd, seed=seed, extra_blocks=B + 2,
+                  max_blocks=max(-(-L // 16) for L in lens) + 1)
+    used = set(sc.block_table[b, i] for b in range(B) for i in range(-(-lens[b] // 16)))
+    free = [i for i in range(sc.num_blocks) if i not in used]
+    table = sc.block_table.copy()
+    slots = []
+    for b, L in enumerate(lens):
+        if L % 16 == 0:
+            table[b, L // 16] = free.pop()
+        slots.append(int(table[b, L // 16]) * 16 + L % 16)
+    g = torch.Generator().manual_seed(seed)
+    k = torch.randn((B, Hkv, 128), generator=g).to(torch.bfloat16)
+    v = torch.randn((B, Hkv, 128), generator=g).to(torch.bfloat16)
+    q = torch.randn((B, Hq, 128), generator=g).to(torch.bfloat16)
+    lens1 = np.asarray(lens, np.int32) + 1
+    cache = PagedKVCache(KVCacheSpec(Hkv, kv_dtype=NAMES[kvd]), sc.num_blocks, device=cuda,
+                         pool=torch.from_numpy(sc.pool).to(cuda))
+    pps = None if rng.random() < 0.5 else int(rng.integers(1, 40))
+    out = decode_step(cache, k.to(cuda), v.to(cuda), torch.tensor(slots, dtype=torch.int32, device=cuda),
+                      q.to(cuda), torch.from_numpy(table).to(cuda), torch.from_numpy(lens1).to(cuda),
+                      out_dtype=torch.float32, pages_per_split=pps, append_tail_only=bool(seed % 3 == 0))
+    pool = sc.pool.copy()
+    O.quant_append(bf16_bits(k), bf16_bits(v), np.asarray(slots, np.int32), kvd, pool)
+    assert np.array_equal(cache.pool.cpu().numpy(), pool)
+    ref = O.decode_attn(bf16_bits(q), pool, table, lens1, Hkv, kvd)
+    assert rel_err(out.cpu().numpy(), ref) <= 2e-3, (lens, Hq, Hkv, kvd, pps)

@@ -69,8 +69,8 @@ int kvq_quant_append(const void* k, const void* v, int64_t k_token_stride,
  * (offset 0, round_up(B * Hkv * 4, 256) bytes) used by the fused split-KV
  * combine, then the split partials (fp32 O + LSE).  The counter region must be
  * zero on entry; the kernel leaves it zero again (graph-replay safe).  When a
- * workspace is reused for a larger B * Hkv, re-zero the grown counter prefix:
- * it overlaps the previous call's partials. */
+ * workspace is reused for a larger B * Hkv than the PREVIOUS call's, re-zero
+ * the counter prefix: beyond the previous call's counters lie its partials. */
 size_t kvq_decode_workspace_bytes(int32_t B, int32_t Hq, int32_t Hkv, int32_t max_splits);
 
 /* Split-KV geometry: pages per split chosen for a workload of `B` sequences,

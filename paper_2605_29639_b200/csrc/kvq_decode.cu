@@ -888,12 +888,35 @@ __device__ __forceinline__ void decode_cta(const DecodeParams& p, uint8_t* smem)
   if constexpr (PEER) peer_signal(p.peer);
 }
 
+#ifdef KVQ_TIMELINE
+// Debug builds only (tools/timeline.py): per-CTA start / end %globaltimer and SM id.
+__device__ unsigned long long g_timeline[1 << 17][3];
+#endif
+
 template <int KVD, bool HI, int MODE>
 __global__ void __launch_bounds__(THREADS, Geo<HI>::CTAS) decode_kernel(const DecodeParams p) {
   extern __shared__ __align__(128) uint8_t smem[];
+#ifdef KVQ_TIMELINE
+  unsigned long long t0 = 0;
+  if (threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+#endif
   if (MODE == 2 && threadIdx.x == 0) peer_release(p.peer);
   decode_cta<KVD, HI, MODE>(p, smem);
   if (MODE == 2 && threadIdx.x == 0) peer_arrive(p.peer);
+#ifdef KVQ_TIMELINE
+  if (threadIdx.x == 0) {
+    unsigned long long t1;
+    unsigned sm;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+    const size_t i = blockIdx.x + (size_t)gridDim.x * (blockIdx.y + (size_t)gridDim.y * blockIdx.z);
+    if (i < (1 << 17)) {
+      g_timeline[i][0] = t0;
+      g_timeline[i][1] = t1;
+      g_timeline[i][2] = sm;
+    }
+  }
+#endif
 }
 
 }  // namespace kvq
@@ -1176,5 +1199,11 @@ int kvq_decode_attn(const void* q, int64_t q_batch_stride, const void* pool, int
                             B, Hq, Hkv, kv_dtype, sm_scale, pages_per_split, workspace, workspace_bytes,
                             out, out_dtype, out_layout, stream);
 }
+
+#ifdef KVQ_TIMELINE
+int kvq_debug_timeline(void* host, size_t bytes) {
+  return cudaMemcpyFromSymbol(host, kvq::g_timeline, bytes) == cudaSuccess ? 0 : -3;
+}
+#endif
 
 }  // extern "C"

@@ -55,7 +55,7 @@ def main():
                                       vp, ctypes.c_size_t, vp, i32, i32, vp]
         import os
         pps = int(os.environ.get("PPS", 0)) or L.kvq_decode_pages_per_split(B, Hkv, NB, mb)
-        wsb = L.kvq_decode_workspace_bytes(B, Hq, Hkv, -(-mb // pps))
+        wsb = L.kvq_decode_workspace_bytes(B, Hq, Hkv, -(-mb // pps) * int(os.environ.get("WSX", 1)))
         ws = torch.zeros(wsb, dtype=torch.uint8, device=dev)
 
         def launch(L=L, pps=pps, ws=ws, wsb=wsb):

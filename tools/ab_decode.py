@@ -11,6 +11,7 @@ from one CUDA graph (GPU time without host launch cost); PPS=n forces the
 split size.
 """
 import ctypes
+import os
 import sys
 
 import numpy as np
@@ -32,7 +33,8 @@ def main():
         pool[..., :4096] &= 0xF7  # no NaN E4M3 codes
     sc = torch.full((NB, Hkv, 32), 0.02, dtype=torch.float32, device=dev)
     pool[..., 4096:] = sc.view(torch.uint8).view(NB, Hkv, 128)
-    perm = np.random.default_rng(7).permutation(NB).astype(np.int32)
+    perm = (np.random.default_rng(7).permutation(NB) if os.environ.get("PERM", "1") != "0"
+            else np.arange(NB)).astype(np.int32)  # PERM=0: contiguous block ids
     table = np.zeros((B, mb), np.int32)
     pos = 0
     for b in range(B):
@@ -53,7 +55,6 @@ def main():
         vp, i32, i64 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64
         L.kvq_decode_attn.argtypes = [vp, i64, vp, i64, vp, i32, vp, i32, i32, i32, i32, ctypes.c_float, i32,
                                       vp, ctypes.c_size_t, vp, i32, i32, vp]
-        import os
         pps = int(os.environ.get("PPS", 0)) or L.kvq_decode_pages_per_split(B, Hkv, NB, mb)
         wsb = L.kvq_decode_workspace_bytes(B, Hq, Hkv, -(-mb // pps) * int(os.environ.get("WSX", 1)))
         ws = torch.zeros(wsb, dtype=torch.uint8, device=dev)
@@ -66,7 +67,6 @@ def main():
         launch()
         runs.append((path, launch, []))
     torch.cuda.synchronize()
-    import os
     if os.environ.get("GRAPH"):  # time 20 launches captured in one CUDA graph: GPU time, no host cost
         graphed = []
         for path, launch, times in runs:

@@ -316,9 +316,13 @@ def run_ours(args, cfg):
             gather_mode = f"nccl (peer setup failed: {type(e).__name__})"
     use_nccl = world > 1 and peer is None
     # The stationary step re-appends each sequence's newest token (its last page).
+    # --append fused: no K1 launch, the K2 CTA holding each sequence's last page
+    # quantizes the new row (KVQ_STEP_FUSED_APPEND); not combined with the peer gather.
+    fused = args.append == "fused" and peer is None
+    l2_fits = cache.nbytes() * world <= 4 * 126e6
     sess = DecodeSession(cache, table_d, B_loc, Hq_loc, total_pages=total_pages, head_major=True,
                          gather_factory=make_gather if use_nccl else None, peer=peer,
-                         pages_per_split=args.pages_per_split, append_tail_only=True)
+                         pages_per_split=args.pages_per_split, append_tail_only=True, fused_append=fused)
     buf = sess.device_buffers(0)
     for name, t in (("q", q), ("k", k_new), ("v", v_new), ("slots", slots_step), ("lens", seq_lens_d)):
         buf[name].copy_(t)
@@ -349,18 +353,36 @@ def run_ours(args, cfg):
     # Event-record nodes cost a few microseconds of launch bubble each, so
     # only every k2_every-th step brackets its K2 (the per-launch sample).
     k2_every = max(1, args.k2_sample_every)
+    # A pool that fits in L2 (C1) would be timed L2-resident: instead every step
+    # is preceded by a 256 MB memset that evicts L2 and bracketed by its own
+    # events (the flush is outside the brackets); ms_step is their mean.
+    flush_buf = torch.empty(256 << 20, dtype=torch.uint8, device=dev) if l2_fits else None
+    step_evs = []
 
     def capture_steps(n, timed):
         evs = {}
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g):
             for i in range(n):
-                if timed and i % k2_every == 0:  # sampled step: K1, event, K2, event
-                    sess.k1(buf)
+                if flush_buf is not None:
+                    flush_buf.zero_()
+                if flush_buf is not None and timed and i % k2_every != 0:
+                    ev = (torch.cuda.Event(enable_timing=True, external=True),
+                          torch.cuda.Event(enable_timing=True, external=True))
+                    ev[0].record()
+                    sess.step(buf)
+                    ev[1].record()
+                    step_evs.append(ev)
+                elif timed and i % k2_every == 0:  # sampled step: K1, event, K2, event
+                    if not fused:
+                        sess.k1(buf)
                     evs[i] = (torch.cuda.Event(enable_timing=True, external=True),
                               torch.cuda.Event(enable_timing=True, external=True))
                     evs[i][0].record()
-                    sess.k2(buf)
+                    if fused:
+                        sess.step(buf)  # the fused step is one K2 launch
+                    else:
+                        sess.k2(buf)
                     evs[i][1].record()
                 else:                            # kvq_decode_step: K2 PDL-launched behind K1
                     sess.step(buf)
@@ -418,6 +440,8 @@ def run_ours(args, cfg):
         torch.cuda.synchronize()
     ms_total = max_over_ranks(t_start.elapsed_time(t_end))
     ms_step = ms_total / args.steps
+    if step_evs:  # L2-flushed steps: the mean bracketed step, not the graph span (which holds the flushes)
+        ms_step = max_over_ranks(statistics.mean(a.elapsed_time(b) for a, b in step_evs))
     k2_ms = statistics.mean(a.elapsed_time(b) for a, b in evs)
     k2_ms = max_over_ranks(k2_ms)
 
@@ -429,7 +453,7 @@ def run_ours(args, cfg):
     es = DecodeSession(cache, table_d, B_loc, Hq_loc, total_pages=total_pages, head_major=True,
                        gather_factory=make_gather if use_nccl else None, peer=peer,
                        pages_per_split=args.pages_per_split, graphs=not (one_gpu and use_nccl),
-                       append_tail_only=True)
+                       append_tail_only=True, fused_append=fused)
     host_inputs = {"q": q, "k": k_new, "v": v_new, "slots": slots_step, "lens": seq_lens_d}
     for b in es.bufs:
         for name, t in host_inputs.items():
@@ -443,14 +467,28 @@ def run_ours(args, cfg):
         e2e_step()
     es.synchronize()
     barrier()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(es.h2d)
-    for _ in range(args.steps):
-        e2e_step()
-    e1.record(es.d2h)
-    es.synchronize()
-    torch.cuda.synchronize()
-    e2e_ms = max_over_ranks(e0.elapsed_time(e1)) / args.steps
+    if flush_buf is None:
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(es.h2d)
+        for _ in range(args.steps):
+            e2e_step()
+        e1.record(es.d2h)
+        es.synchronize()
+        torch.cuda.synchronize()
+        e2e_ms = max_over_ranks(e0.elapsed_time(e1)) / args.steps
+    else:  # L2 flushed before every step: serialized per-step latency, upload to download
+        tot = 0.0
+        for _ in range(args.steps):
+            flush_buf.zero_()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(es.h2d)
+            e2e_step()
+            e1.record(es.d2h)
+            es.synchronize()
+            torch.cuda.synchronize()
+            tot += e0.elapsed_time(e1)
+        e2e_ms = max_over_ranks(tot / args.steps)
     h2d = es.in_bytes
     d2h = o_h.numel() * o_h.element_size()
 
@@ -502,7 +540,10 @@ def run_ours(args, cfg):
                                    f"{plan.h_split} kv-head groups x {plan.b_split} LPT batch parts")
                    if world > 1 else "1 GPU",
                    "l2": "inputs larger than L2 (pool %.2f GB vs 126 MB L2); no flush" % (cache.nbytes() * world / 1e9)
-                   if cache.nbytes() * world > 4 * 126e6 else "pool fits in L2: L2-resident numbers",
+                   if not l2_fits else "pool fits in L2: a 256 MB memset evicts L2 before every step (outside the "
+                                       "step's event brackets); value and e2e are per-step means of flushed steps",
+                   "append": "fused into K2 (KVQ_STEP_FUSED_APPEND: no K1 launch)" if fused
+                   else "K1 + K2 (PDL, tail-only wait)",
                    "step": "K1 append of B rows + K2 paged decode attention (+ the gather if N>1); "
                            "stationary ctx; the K timed steps are one CUDA graph (kvq_decode_step per step: K2 "
                            "launched behind K1 with programmatic dependent launch, waiting for K1 only before "
@@ -521,7 +562,7 @@ def run_ours(args, cfg):
                      else "fallback 6.65 TB/s (B200_PROFILING.md)"},
         "e2e": {"value": B / (e2e_ms * 1e-3), "unit": "tokens/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms},
-        "gpu_launches": 2 * args.steps,
+        "gpu_launches": (1 if fused else 2) * args.steps,
         "clocks": sampler.summary(),
     }
     if cpu is not None:
@@ -702,6 +743,9 @@ def main(argv=None):
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--pages-per-split", type=int, default=None,
                     help="override the split-KV geometry (default: kvq_decode_pages_per_split)")
+    ap.add_argument("--append", default="pdl", choices=["pdl", "fused"],
+                    help="C1-C4: append the step's new rows with K1 + PDL-launched K2 (pdl) or inside K2 "
+                         "(fused: no K1 launch; 1 GPU / NCCL gather only)")
     ap.add_argument("--gather", default="peer", choices=["peer", "nccl"],
                     help="N > 1: fuse the KV-head output all-gather into K2 over peer memory (default) "
                          "or run NCCL all_gather_into_tensor after K2")

@@ -185,6 +185,12 @@ int kvq_decode_attn_peer(const void* q, int64_t q_batch_stride, const void* pool
  * Replaces the decode-step pair the reference charges as one constant,
  * simulator.py:499-517. */
 #define KVQ_STEP_APPEND_TAIL_ONLY 1
+/* flags & KVQ_STEP_FUSED_APPEND: no K1 launch.  The caller promises T == B and
+ * that row b of k / v is sequence b's newest token: position seq_lens[b] - 1,
+ * slot_mapping[b] its slot in block_table[b] (a plain decode step).  The K2 CTA
+ * holding that page quantizes the row (K1's rounding contract, bit-identical),
+ * writes it to the pool and attends over it.  q_len == 1, no peer gather. */
+#define KVQ_STEP_FUSED_APPEND 2
 int kvq_decode_step(const void* k, const void* v, int64_t k_token_stride, int64_t v_token_stride,
                     const int32_t* slot_mapping, int32_t T, const void* q, int64_t q_batch_stride,
                     void* pool, int64_t num_blocks, const int32_t* block_table, int32_t max_blocks,

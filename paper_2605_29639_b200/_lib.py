@@ -19,6 +19,7 @@ KVQ_INT8, KVQ_FP8_E4M3 = 0, 1
 KVQ_OUT_BF16, KVQ_OUT_F32 = 0, 1
 KVQ_OUT_BHD, KVQ_OUT_HBD = 0, 1
 KVQ_STEP_APPEND_TAIL_ONLY = 1
+KVQ_STEP_FUSED_APPEND = 2
 HEAD_DIM = 128
 BLOCK_SIZE = 16
 PAGE_BYTES = 4224

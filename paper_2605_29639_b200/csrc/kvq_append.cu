@@ -272,27 +272,6 @@ constexpr int K1R_WARPS = 8;
 constexpr int64_t K1_ROWS_MAX = 8192;
 
 template <int KVD>
-__device__ __forceinline__ uint32_t codes4(const float (&x)[4], float inv) {
-  float y[4];
-#pragma unroll
-  for (int e = 0; e < 4; ++e) y[e] = __fmul_rn(x[e], inv);
-  if constexpr (KVD == KVQ_FP8_E4M3) {
-    uint16_t l, h;
-    asm("cvt.rn.satfinite.e4m3x2.f32 %0, %1, %2;" : "=h"(l) : "f"(y[1]), "f"(y[0]));
-    asm("cvt.rn.satfinite.e4m3x2.f32 %0, %1, %2;" : "=h"(h) : "f"(y[3]), "f"(y[2]));
-    return (uint32_t)l | ((uint32_t)h << 16);
-  } else {
-    uint32_t word = 0;
-#pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      const int c = max(-127, min(127, __float2int_rn(y[e])));  // NaN -> 0, saturating
-      word |= ((uint32_t)(c & 0xff)) << (8 * e);
-    }
-    return word;
-  }
-}
-
-template <int KVD>
 __global__ void __launch_bounds__(K1R_WARPS * 32) quant_append_rows_kernel(
     const __nv_bfloat16* __restrict__ k, const __nv_bfloat16* __restrict__ v, int64_t k_stride,
     int64_t v_stride, const int32_t* __restrict__ slots, int T, int Hkv,
@@ -323,7 +302,7 @@ __global__ void __launch_bounds__(K1R_WARPS * 32) quant_append_rows_kernel(
   const float qmax = KVD == KVQ_FP8_E4M3 ? 448.0f : 127.0f;
   const float ik = ak > 0.0f ? __fdiv_rn(qmax, ak) : 0.0f;
   const float iv = av > 0.0f ? __fdiv_rn(qmax, av) : 0.0f;
-  const uint32_t ck = codes4<KVD>(xk, ik), cv = codes4<KVD>(xv, iv);
+  const uint32_t ck = quant_codes4<KVD>(xk, ik), cv = quant_codes4<KVD>(xv, iv);
   const int tok = slot & 15;
   uint8_t* page = pool + ((int64_t)(slot >> 4) * Hkv + h) * PAGE;
   *reinterpret_cast<uint32_t*>(page + k_code_off(tok, 4 * lane)) = ck;

@@ -149,6 +149,30 @@ __device__ __forceinline__ float fast_exp2(float x) {
   return y;
 }
 
+// Codes of 4 consecutive values of one row (contract): y = x * inv
+// (RN, never contracted); INT8 rint_even + clamp (NaN -> 0), FP8 satfinite RNE.
+// Shared by K1's one-warp-per-row kernel and K2's fused append (bit-identical).
+template <int KVD>
+__device__ __forceinline__ uint32_t quant_codes4(const float (&x)[4], float inv) {
+  float y[4];
+#pragma unroll
+  for (int e = 0; e < 4; ++e) y[e] = __fmul_rn(x[e], inv);
+  if constexpr (KVD == KVQ_FP8_E4M3) {
+    uint16_t l, h;
+    asm("cvt.rn.satfinite.e4m3x2.f32 %0, %1, %2;" : "=h"(l) : "f"(y[1]), "f"(y[0]));
+    asm("cvt.rn.satfinite.e4m3x2.f32 %0, %1, %2;" : "=h"(h) : "f"(y[3]), "f"(y[2]));
+    return (uint32_t)l | ((uint32_t)h << 16);
+  } else {
+    uint32_t word = 0;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int c = max(-127, min(127, __float2int_rn(y[e])));  // NaN -> 0, saturating
+      word |= ((uint32_t)(c & 0xff)) << (8 * e);
+    }
+    return word;
+  }
+}
+
 // 8-bit codes -> two f16x2 registers (exact for every INT8 / E4M3 code).
 // Input bytes (b0, b1, b2, b3) -> lo = (b0, b1), hi = (b2, b3).  With
 // BIASED (INT8 only) the values are code + 1152 and the caller removes the

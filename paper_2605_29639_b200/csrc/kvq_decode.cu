@@ -36,6 +36,13 @@ struct DecodeParams {
   int out_f32, out_hbd;
   kvq_peer_out peer;    // n_peers == 0: local output only (no fused gather)
   int tail_only;        // behind K1 (PDL): K1's rows lie only in each sequence's last page
+  // MODE 3 (kvq_decode_step with KVQ_STEP_FUSED_APPEND): row b of ak / av is
+  // sequence b's newest token (position seq_lens[b] - 1, slot aslots[b]); the
+  // CTA holding that page quantizes it (K1's contract) instead of a K1 launch.
+  const __nv_bfloat16* ak;
+  const __nv_bfloat16* av;
+  int64_t ak_stride, av_stride;
+  const int32_t* aslots;
 };
 
 constexpr int NW = 4;  // warps per CTA; every warp streams its own pages
@@ -51,6 +58,7 @@ struct Geo {
   // one conflict-free LDS.64 per k-step) so the live set fits 128 registers.
   static constexpr size_t QSM = HI ? (size_t)NT * 8 * 32 * 8 : 0;  // [nt][k-step pair][lane] uint4
   static constexpr size_t SMEM = (size_t)NW * S * PAGE + QSM + NW * S * sizeof(uint64_t) + 16;
+  static constexpr size_t PATCH = 32 * 8 + 16;  // MODE 3: the appended row's codes + scales
   static_assert((size_t)NW * S * PAGE >= (size_t)NW * 16 * HD * 4 + 2 * NW * 16 * 4,
                 "merge scratch must fit in the ring");
 };
@@ -243,7 +251,7 @@ struct PageStream {
 // MODE: 0 = decode, 1 = multi-query (q_len > 1), 2 = decode with the fused peer gather.
 template <int KVD, bool HI, int MODE>
 __device__ __forceinline__ void decode_cta(const DecodeParams& p, uint8_t* smem) {
-  constexpr bool MQ = MODE == 1, PEER = MODE == 2;
+  constexpr bool MQ = MODE == 1, PEER = MODE == 2, FUSED = MODE == 3;
   constexpr int NT = Geo<HI>::NT;
   constexpr int S = Geo<HI>::S;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + NW * S * PAGE);
@@ -321,6 +329,51 @@ __device__ __forceinline__ void decode_cta(const DecodeParams& p, uint8_t* smem)
   }
 #pragma unroll 1
   for (int j = 0; j < S && j < ps.nj; ++j) ps.issue(j, lane, j);
+
+  // MODE 3: the warp that owns the sequence's last page quantizes the new row
+  // (one warp per row, lane l: d [4l, 4l+4), exactly K1's rows kernel), stores
+  // it to the pool for later steps, and keeps it in shared memory to patch into
+  // its copy of that page when it lands (the bulk copy may read the old bytes).
+  int patch_j = -1, ptok = 0;
+  uint32_t* patch = reinterpret_cast<uint32_t*>(smem + NW * S * PAGE + NW * S * sizeof(uint64_t) + 16 +
+                                                Geo<HI>::QSM);
+  if constexpr (FUSED) {
+    const int last = npages - 1 - pg0;
+    if (last >= 0 && last < n && last % NW == warp) {
+      patch_j = last / NW;
+      ptok = (L - 1) & (BS - 1);
+      const uint2 kw = __ldg(reinterpret_cast<const uint2*>(p.ak + (int64_t)b * p.ak_stride + h * HD + 4 * lane));
+      const uint2 vw = __ldg(reinterpret_cast<const uint2*>(p.av + (int64_t)b * p.av_stride + h * HD + 4 * lane));
+      const int aslot = __ldg(p.aslots + b);
+      const float xk[4] = {__uint_as_float(kw.x << 16), __uint_as_float(kw.x & 0xffff0000u),
+                           __uint_as_float(kw.y << 16), __uint_as_float(kw.y & 0xffff0000u)};
+      const float xv[4] = {__uint_as_float(vw.x << 16), __uint_as_float(vw.x & 0xffff0000u),
+                           __uint_as_float(vw.y << 16), __uint_as_float(vw.y & 0xffff0000u)};
+      float ak = fmaxf(fmaxf(fabsf(xk[0]), fabsf(xk[1])), fmaxf(fabsf(xk[2]), fabsf(xk[3])));
+      float av = fmaxf(fmaxf(fabsf(xv[0]), fabsf(xv[1])), fmaxf(fabsf(xv[2]), fabsf(xv[3])));
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        ak = fmaxf(ak, __shfl_xor_sync(FULL, ak, o));
+        av = fmaxf(av, __shfl_xor_sync(FULL, av, o));
+      }
+      const float qmax = KVD == KVQ_FP8_E4M3 ? 448.0f : 127.0f;
+      const uint32_t ck = quant_codes4<KVD>(xk, ak > 0.0f ? __fdiv_rn(qmax, ak) : 0.0f);
+      const uint32_t cv = quant_codes4<KVD>(xv, av > 0.0f ? __fdiv_rn(qmax, av) : 0.0f);
+      const float sc = __fdiv_rn(lane ? av : ak, qmax);  // lanes 0 / 1: K / V scale
+      patch[2 * lane] = ck;
+      patch[2 * lane + 1] = cv;
+      if (lane < 2) patch[64 + lane] = __float_as_uint(sc);
+      if (aslot >= 0 && (aslot >> 4) < p.num_blocks) {
+        uint8_t* page = const_cast<uint8_t*>(p.pool) + ((int64_t)(aslot >> 4) * p.Hkv + h) * PAGE;
+        const int tok = aslot & 15;
+        *reinterpret_cast<uint32_t*>(page + k_code_off(tok, 4 * lane)) = ck;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) page[v_code_off(tok, 4 * lane + e)] = (uint8_t)(cv >> (8 * e));
+        if (lane < 2) *reinterpret_cast<float*>(page + (lane ? VS_OFF : KS_OFF) + 4 * tok) = sc;
+      }
+      __syncwarp();
+    }
+  }
 
   const int r = lane >> 2, c = lane & 3;
 
@@ -465,6 +518,20 @@ __device__ __forceinline__ void decode_cta(const DecodeParams& p, uint8_t* smem)
   for (int j = 0; j < ps.nj; ++j) {
     mbar_wait(&ps.full[slot], phase);
     const uint32_t pgs = ring_s + slot * PAGE;
+    if (FUSED && j == patch_j) {  // the new row over the copy's (possibly stale) bytes
+      const uint32_t cv = patch[2 * lane + 1];
+      asm volatile("st.shared.b32 [%0], %1;" ::"r"(pgs + k_code_off(ptok, 4 * lane)), "r"(patch[2 * lane]) : "memory");
+#pragma unroll
+      for (int e = 0; e < 4; ++e)
+        asm volatile("st.shared.u8 [%0], %1;" ::"r"(pgs + v_code_off(ptok, 4 * lane + e)), "r"((cv >> (8 * e)) & 0xffu)
+                     : "memory");
+      if (lane < 2)
+        asm volatile("st.shared.b32 [%0], %1;" ::"r"(pgs + (lane ? VS_OFF : KS_OFF) + 4 * ptok), "r"(patch[64 + lane])
+                     : "memory");
+      // generic-proxy writes into a slot the bulk copy will refill later
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncwarp();
+    }
     const uint4 k0 = lds128_at<0>(pgs + kb02), k2 = lds128_at<128>(pgs + kb02);
     const uint4 k1 = lds128_at<0>(pgs + kb13), k3 = lds128_at<128>(pgs + kb13);
     uint4 v0, v1, v2, v3;
@@ -1023,7 +1090,9 @@ static int decode_attn_impl(const void* q, int64_t q_batch_stride, int32_t q_len
                             const int32_t* seq_lens, int32_t B, int32_t Hq, int32_t Hkv, int32_t kv_dtype,
                             float sm_scale, int32_t pages_per_split, void* workspace,
                             size_t workspace_bytes, void* out, int32_t out_dtype, int32_t out_layout,
-                            const kvq_peer_out* peer, void* stream, bool pdl = false, bool tail_only = false) {
+                            const kvq_peer_out* peer, void* stream, bool pdl = false, bool tail_only = false,
+                            const void* fk = nullptr, const void* fv = nullptr, int64_t fk_stride = 0,
+                            int64_t fv_stride = 0, const int32_t* fslots = nullptr) {
   if (B < 0 || Hq <= 0 || Hkv <= 0 || max_blocks <= 0 || num_blocks <= 0 || q_len <= 0)
     return fail(KVQ_EINVAL, "decode_attn: bad sizes");
   if (B == 0) return KVQ_OK;
@@ -1077,11 +1146,17 @@ static int decode_attn_impl(const void* q, int64_t q_batch_stride, int32_t q_len
   prm.peer = kvq_peer_out{};
   if (peer) prm.peer = *peer;
   prm.tail_only = pdl && tail_only;
+  const bool fused = fk != nullptr;
+  prm.ak = static_cast<const __nv_bfloat16*>(fk);
+  prm.av = static_cast<const __nv_bfloat16*>(fv);
+  prm.ak_stride = fk_stride;
+  prm.av_stride = fv_stride;
+  prm.aslots = fslots;
 
   const dim3 grid((unsigned)max_splits, (unsigned)Hkv, (unsigned)B);
   auto st = static_cast<cudaStream_t>(stream);
   const bool hi = prm.G > 8;
-  const size_t smem_bytes = hi ? kvq::Geo<true>::SMEM : kvq::Geo<false>::SMEM;
+  const size_t smem_bytes = (hi ? kvq::Geo<true>::SMEM : kvq::Geo<false>::SMEM) + (fused ? kvq::Geo<false>::PATCH : 0);
   auto launch = [&](auto kernel) -> int {
     cudaError_t e = set_attributes_once(reinterpret_cast<const void*>(kernel), (int)smem_bytes);
     if (e != cudaSuccess) return fail(KVQ_ECUDA, cudaGetErrorString(e));
@@ -1099,7 +1174,12 @@ static int decode_attn_impl(const void* q, int64_t q_batch_stride, int32_t q_len
     if (e != cudaSuccess) return fail(KVQ_ECUDA, cudaGetErrorString(e));
     return check_launch("decode_attn");
   };
-  const int mode = peer ? 2 : (q_len > 1 ? 1 : 0);
+  const int mode = fused ? 3 : peer ? 2 : (q_len > 1 ? 1 : 0);
+  if (mode == 3) {
+    if (kv_dtype == KVQ_INT8)
+      return hi ? launch(kvq::decode_kernel<KVQ_INT8, true, 3>) : launch(kvq::decode_kernel<KVQ_INT8, false, 3>);
+    return hi ? launch(kvq::decode_kernel<KVQ_FP8_E4M3, true, 3>) : launch(kvq::decode_kernel<KVQ_FP8_E4M3, false, 3>);
+  }
   if (kv_dtype == KVQ_INT8) {
     if (mode == 2) return hi ? launch(kvq::decode_kernel<KVQ_INT8, true, 2>) : launch(kvq::decode_kernel<KVQ_INT8, false, 2>);
     if (mode == 1) return hi ? launch(kvq::decode_kernel<KVQ_INT8, true, 1>) : launch(kvq::decode_kernel<KVQ_INT8, false, 1>);
@@ -1119,8 +1199,24 @@ int kvq_decode_step_mq(const void* k, const void* v, int64_t k_token_stride, int
                        int32_t kv_dtype, float sm_scale, int32_t pages_per_split, void* workspace,
                        size_t workspace_bytes, void* out, int32_t out_dtype, int32_t out_layout,
                        const kvq_peer_out* peer, int32_t flags, void* stream) {
-  if (flags & ~KVQ_STEP_APPEND_TAIL_ONLY) return fail(KVQ_EINVAL, "decode_step: unknown flags");
+  if (flags & ~(KVQ_STEP_APPEND_TAIL_ONLY | KVQ_STEP_FUSED_APPEND)) return fail(KVQ_EINVAL, "decode_step: unknown flags");
   if (q_len <= 0) return fail(KVQ_EINVAL, "decode_step: bad q_len");
+  if (flags & KVQ_STEP_FUSED_APPEND) {
+    // No K1 launch: K2's CTA holding each sequence's last page quantizes the row.
+    if (q_len != 1 || peer || T != B)
+      return fail(KVQ_EINVAL, "decode_step: KVQ_STEP_FUSED_APPEND needs q_len == 1, no peer gather and T == B");
+    if (kv_dtype != KVQ_INT8 && kv_dtype != KVQ_FP8_E4M3)
+      return fail(KVQ_EUNSUPPORTED, "decode_step: unknown kv dtype");
+    if (B > 0 && (!k || !v || !slot_mapping))
+      return fail(KVQ_EINVAL, "decode_step: null pointer");
+    if (!aligned(k, 8) || !aligned(v, 8) || (k_token_stride % 4) || (v_token_stride % 4) ||
+        k_token_stride < (int64_t)Hkv * KVQ_HEAD_DIM || v_token_stride < (int64_t)Hkv * KVQ_HEAD_DIM)
+      return fail(KVQ_EINVAL, "decode_step: k/v rows must be 8-byte aligned with a token stride >= Hkv * 128");
+    return decode_attn_impl(q, q_batch_stride, 1, pool, num_blocks, block_table, max_blocks, seq_lens, B, Hq, Hkv,
+                            kv_dtype, sm_scale, pages_per_split, workspace, workspace_bytes, out, out_dtype,
+                            out_layout, nullptr, stream, false, false, k, v, k_token_stride, v_token_stride,
+                            slot_mapping);
+  }
   if (peer && q_len != 1) return fail(KVQ_EINVAL, "decode_step: the fused gather takes one query token per sequence");
   if (peer && (out_dtype != KVQ_OUT_BF16 || out_layout != KVQ_OUT_HBD))
     return fail(KVQ_EINVAL, "decode_step: the fused gather writes bf16 head-major rows");

@@ -233,7 +233,7 @@ def decode_step(cache: PagedKVCache, k: torch.Tensor, v: torch.Tensor, slot_mapp
                 total_pages: Optional[int] = None, out: Optional[torch.Tensor] = None,
                 out_dtype: torch.dtype = torch.bfloat16, head_major: bool = False,
                 workspace: Optional[torch.Tensor] = None, peer=None, slot: int = 0,
-                append_tail_only: bool = False) -> torch.Tensor:
+                append_tail_only: bool = False, fused_append: bool = False) -> torch.Tensor:
     """One decode step in one call (``kvq_decode_step``): :func:`quantize_append`
     of the new rows, then :func:`paged_decode_attention` (or, with ``peer``,
     :func:`paged_decode_attention_gathered`), with K2 launched behind K1 by
@@ -248,7 +248,13 @@ def decode_step(cache: PagedKVCache, k: torch.Tensor, v: torch.Tensor, slot_mapp
     ``q`` of shape ``[B, q_len, Hq, 128]`` makes it a speculative-decoding
     verify step (``kvq_decode_step_mq``): the ``q_len`` draft tokens' rows are
     appended and scored causally, as :func:`paged_decode_attention` does for a
-    4-D ``q`` (``append_tail_only`` does not apply; no ``peer``)."""
+    4-D ``q`` (``append_tail_only`` does not apply; no ``peer``).
+
+    ``fused_append=True`` (``KVQ_STEP_FUSED_APPEND``) launches no K1: row b of
+    ``k`` / ``v`` must be sequence b's newest token (position
+    ``seq_lens[b] - 1``, slot ``slot_mapping[b]``), and the K2 CTA holding that
+    page quantizes it itself -- same pool bytes and output as the two calls.
+    One query token per sequence, no ``peer``."""
     _check_append("decode_step", cache, k, v, slot_mapping)
     _require_cuda("decode_step", q, block_table, seq_lens)
     spec = cache.spec
@@ -260,6 +266,9 @@ def decode_step(cache: PagedKVCache, k: torch.Tensor, v: torch.Tensor, slot_mapp
     q_len = q.shape[1] if multi else 1
     if multi and (q.stride(1) != Hq * 128 or peer is not None):
         raise ValueError("decode_step: multi-query q needs contiguous tokens and no peer gather")
+    if fused_append and (multi or peer is not None or k.shape[0] != B):
+        raise ValueError("decode_step: fused_append needs one new row per sequence (T == B), "
+                         "one query token and no peer gather")
     if block_table.dtype != torch.int32 or block_table.dim() != 2 or block_table.shape[0] != B \
             or not block_table.is_contiguous():
         raise ValueError("decode_step: block_table must be contiguous int32 [B, max_blocks]")
@@ -300,7 +309,8 @@ def decode_step(cache: PagedKVCache, k: torch.Tensor, v: torch.Tensor, slot_mapp
         workspace.data_ptr(), workspace.numel() * workspace.element_size(), out.data_ptr(),
         _lib.KVQ_OUT_F32 if out_dtype == torch.float32 else _lib.KVQ_OUT_BF16,
         _lib.KVQ_OUT_HBD if head_major else _lib.KVQ_OUT_BHD, desc,
-        _lib.KVQ_STEP_APPEND_TAIL_ONLY if append_tail_only else 0, _stream_handle(q.device))
+        (_lib.KVQ_STEP_APPEND_TAIL_ONLY if append_tail_only else 0)
+        | (_lib.KVQ_STEP_FUSED_APPEND if fused_append else 0), _stream_handle(q.device))
     _lib.check("kvq_decode_step", st)
     return out
 

@@ -35,7 +35,7 @@ class DecodeSession:
                  *, total_pages: Optional[int] = None, out_dtype: torch.dtype = torch.bfloat16,
                  head_major: bool = False, sm_scale: Optional[float] = None, depth: int = 2,
                  gather_factory=None, pages_per_split: Optional[int] = None, graphs: bool = False,
-                 peer=None, append_tail_only: bool = False):
+                 peer=None, append_tail_only: bool = False, fused_append: bool = False):
         """With ``gather_factory`` (returning a
         :class:`paper_2605_29639_b200.shard.OutputGather`, one per buffer slot,
         for KV-head / 2-D sharding) the local head-major output
@@ -49,7 +49,10 @@ class DecodeSession:
 
         ``append_tail_only=True`` promises that each step's slots are the
         sequences' newest tokens (in their last page): K2 then streams every
-        other page while K1 runs (``ops.decode_step``).
+        other page while K1 runs (``ops.decode_step``).  ``fused_append=True``
+        makes the same promise with one row per sequence (row b = sequence b's
+        newest token) and launches no K1 at all: K2 quantizes the rows itself
+        (``KVQ_STEP_FUSED_APPEND``; ignored with ``peer``).
 
         With ``graphs=True`` each buffer slot's device work (K1, K2 and the
         gather) is captured once as a CUDA graph on first use and replayed by
@@ -109,6 +112,7 @@ class DecodeSession:
         self.step_idx = 0
         self.graphs = graphs
         self.append_tail_only = append_tail_only
+        self.fused_append = fused_append and peer is None
 
     def k1(self, buf) -> None:
         """Quantize-on-append of the step's new K/V rows (device buffers)."""
@@ -133,7 +137,8 @@ class DecodeSession:
         decode_step(self.cache, buf["k"], buf["v"], buf["slots"], buf["q"], self.block_table, buf["lens"],
                     sm_scale=self.sm_scale, pages_per_split=self.pps, out=buf["out"],
                     out_dtype=self.out_dtype, head_major=self.head_major, workspace=buf["ws"],
-                    peer=self.peer, slot=buf["idx"], append_tail_only=self.append_tail_only)
+                    peer=self.peer, slot=buf["idx"], append_tail_only=self.append_tail_only,
+                    fused_append=self.fused_append)
 
     def _kernels(self, buf, k1: bool = True) -> None:
         if k1:

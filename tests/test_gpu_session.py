@@ -328,3 +328,65 @@ def test_decode_step_speculative_verify(cuda, q_len):
     assert out_a.shape == (B, q_len, Hq, 128)
     assert torch.equal(a.pool, b.pool)
     assert torch.equal(out_a, out_b)
+
+
+@pytest.mark.parametrize("kv_dtype", ["int8", "fp8_e4m3"])
+@pytest.mark.parametrize("Hq,Hkv", [(32, 8), (64, 4)])
+def test_decode_step_fused_append(cuda, kv_dtype, Hq, Hkv):
+    """KVQ_STEP_FUSED_APPEND (no K1 launch; the K2 CTA holding each sequence's
+    last page quantizes its new row) == K1 then K2: identical pool bytes and
+    bit-identical output, eager and replayed from a CUDA graph with new rows,
+    for the g <= 8 and g = 16 variants, including sequences whose new token
+    opens a fresh block."""
+    kvo = O.INT8 if kv_dtype == "int8" else O.FP8_E4M3
+    lens = [300, 17, 1020, 64, 1999, 0, 15]
+    sc = Scenario(lens, Hq, Hkv, kvo, seed=41, extra_blocks=10, max_blocks=max(-(-L // 16) for L in lens) + 1)
+    used = set(sc.block_table[b, i] for b in range(sc.B) for i in range(-(-lens[b] // 16)))
+    free = [i for i in range(sc.num_blocks) if i not in used]
+    table_np = sc.block_table.copy()
+    slots_np = []
+    for b, L in enumerate(lens):
+        if L % 16 == 0:
+            table_np[b, L // 16] = free.pop()
+        slots_np.append(int(table_np[b, L // 16]) * 16 + L % 16)
+    table = torch.from_numpy(table_np).to(cuda)
+    slots = torch.tensor(slots_np, dtype=torch.int32, device=cuda)
+    lens1 = torch.tensor([L + 1 for L in lens], dtype=torch.int32, device=cuda)
+    pool0 = torch.from_numpy(sc.pool).to(cuda)
+    a = PagedKVCache(KVCacheSpec(Hkv, kv_dtype=kv_dtype), sc.num_blocks, device=cuda, pool=pool0.clone())
+    b_ = PagedKVCache(KVCacheSpec(Hkv, kv_dtype=kv_dtype), sc.num_blocks, device=cuda, pool=pool0.clone())
+    g = torch.Generator(device=cuda).manual_seed(6)
+    B = len(lens)
+    k = torch.randn((B, Hkv, 128), device=cuda, generator=g).to(torch.bfloat16)
+    v = torch.randn((B, Hkv, 128), device=cuda, generator=g).to(torch.bfloat16)
+    q = torch.randn((B, Hq, 128), device=cuda, generator=g).to(torch.bfloat16)
+    for pps in (None, 5):
+        out_a = decode_step(a, k, v, slots, q, table, lens1, out_dtype=torch.float32, pages_per_split=pps,
+                            fused_append=True)
+        out_b = decode_step(b_, k, v, slots, q, table, lens1, out_dtype=torch.float32, pages_per_split=pps)
+        torch.cuda.synchronize()
+        assert torch.equal(a.pool, b_.pool)
+        assert torch.equal(out_a, out_b)
+    from paper_2605_29639_b200 import ops
+    nws = ops.workspace_bytes(B, Hq, Hkv, -(-table.shape[1] // 5))
+    ws_a = torch.zeros(nws, dtype=torch.uint8, device=cuda)
+    ws_b = torch.zeros(nws, dtype=torch.uint8, device=cuda)
+    oa = torch.empty((B, Hq, 128), dtype=torch.float32, device=cuda)
+    ob = torch.empty((B, Hq, 128), dtype=torch.float32, device=cuda)
+    ga, gb = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
+    with torch.cuda.graph(ga):
+        decode_step(a, k, v, slots, q, table, lens1, out=oa, out_dtype=torch.float32, pages_per_split=5,
+                    workspace=ws_a, fused_append=True)
+    with torch.cuda.graph(gb):
+        decode_step(b_, k, v, slots, q, table, lens1, out=ob, out_dtype=torch.float32, pages_per_split=5,
+                    workspace=ws_b)
+    for _ in range(3):
+        k.copy_(torch.randn((B, Hkv, 128), device=cuda, generator=g).to(torch.bfloat16))
+        v.copy_(torch.randn((B, Hkv, 128), device=cuda, generator=g).to(torch.bfloat16))
+        ga.replay()
+        gb.replay()
+        torch.cuda.synchronize()
+        assert torch.equal(a.pool, b_.pool)
+        assert torch.equal(oa, ob)
+    with pytest.raises(ValueError):
+        decode_step(a, k[:2], v[:2], slots[:2], q, table, lens1, fused_append=True)

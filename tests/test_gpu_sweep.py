@@ -114,12 +114,14 @@ def test_cached_workspace_across_shapes(cuda):
             assert rel_err(run(sc, cuda, pages_per_split=pps, out=out), ref) <= 2e-3
 
 
+@pytest.mark.parametrize("fused", [False, True])
 @pytest.mark.parametrize("seed", range(12))
-def test_random_decode_steps(cuda, seed):
-    """decode_step (K1 + PDL-launched K2 in one call) on random shapes: the new
-    row of every sequence (opening a fresh block when its last page is full)
-    lands bit-exact where the oracle puts it, and the attention over the
-    grown sequences matches the oracle."""
+def test_random_decode_steps(cuda, seed, fused):
+    """decode_step (K1 + PDL-launched K2 in one call, or K2 alone quantizing
+    the new rows itself with fused_append) on random shapes: the new row of
+    every sequence (opening a fresh block when its last page is full) lands
+    bit-exact where the oracle puts it, and the attention over the grown
+    sequences matches the oracle."""
     from paper_2605_29639_b200 import decode_step
     rng = np.random.default_rng(2000 + seed)
     Hkv = int(rng.choice([1, 2, 4, 8]))
@@ -148,7 +150,8 @@ def test_random_decode_steps(cuda, seed):
     pps = None if rng.random() < 0.5 else int(rng.integers(1, 40))
     out = decode_step(cache, k.to(cuda), v.to(cuda), torch.tensor(slots, dtype=torch.int32, device=cuda),
                       q.to(cuda), torch.from_numpy(table).to(cuda), torch.from_numpy(lens1).to(cuda),
-                      out_dtype=torch.float32, pages_per_split=pps, append_tail_only=bool(seed % 3 == 0))
+                      out_dtype=torch.float32, pages_per_split=pps, append_tail_only=bool(seed % 3 == 0),
+                      fused_append=fused)
     pool = sc.pool.copy()
     O.quant_append(bf16_bits(k), bf16_bits(v), np.asarray(slots, np.int32), kvd, pool)
     assert np.array_equal(cache.pool.cpu().numpy(), pool)

@@ -1015,11 +1015,14 @@ int32_t kvq_decode_pages_per_split(int32_t B, int32_t Hkv, int64_t total_pages, 
   const int64_t work = total_pages * (int64_t)Hkv;
   if (max_blocks > 0 && work <= slots * 128) {
     // Small, latency-bound launch (one wave at 128-page splits): pick the split
-    // size from a cost model fitted to CUDA-graph timings of B = 1..32 shapes
-    // (tools/ab_decode.py GRAPH=1 PPS=...):
-    //   t = waves * (4.5 us + pages_per_cta * t_page) + 0.14 us * (splits - 1),
-    //   t_page = max(concurrent CTAs * 4224 B / 6.9 TB/s, 0.22 us),
-    // the last term being the fused combine (one CTA merges every split).
+    // size from a cost model fitted to cold-L2 timings of B = 1..32 shapes
+    // (tools/ab_decode.py FLUSH=1 PPS=...; each layer's KV is cold in serving):
+    //   t = waves * (6 us + pages_per_cta * t_page) + 0.1 us * (splits - 1)
+    //       + 0.01 us * concurrent CTAs,
+    //   t_page = max(concurrent CTAs * 4224 B / 6.0 TB/s, 0.18 us),
+    // the second term being the fused combine (one CTA merges every split), the
+    // third the dispatch / ramp cost of a wider grid (equal-length batches;
+    // ragged ones below use the first, L2-warm fit).
     static const int cand[] = {8, 9, 10, 12, 14, 16, 19, 22, 26, 30, 35, 41, 48, 56, 64, 75, 88, 103, 120, 140,
                                164, 192, 224, 262, 306, 358, 419, 490, 573, 670, 784, 917, 1073, 1255};
     // Ragged batches (total below B * max_blocks): sum_b ceil(n_b / pps) is
@@ -1038,8 +1041,13 @@ int32_t kvq_decode_pages_per_split(int32_t B, int32_t Hkv, int64_t total_pages, 
       int64_t ctas = pairs0 * ns;
       if (ragged) ctas = std::min(ctas, (int64_t)Hkv * ((total_pages + pps_eff - 1) / pps_eff + (B + 1) / 2));
       const double nw = ragged ? std::max(1.0, (double)ctas / slots) : (double)((ctas + slots - 1) / slots);
-      const double tpage = std::max((double)std::min(ctas, slots) * 4224.0 / 6.9e6, 0.22);
-      const double t = nw * (4.5 + pps_eff * tpage) + 0.14 * (ns - 1);
+      const double conc = (double)std::min(ctas, slots);
+      // Ragged batches keep the first (L2-warm) fit, t_page >= 0.22 us and no
+      // width term: the cold fit over-favours long CTAs there (B = 8 ragged
+      // 26.6 -> 28.7 us), the longest sequence setting the time either way.
+      const double t = ragged ? nw * (4.5 + pps_eff * std::max(conc * 4224.0 / 6.9e6, 0.22)) + 0.14 * (ns - 1)
+                              : nw * (6.0 + pps_eff * std::max(conc * 4224.0 / 6.0e6, 0.18)) + 0.1 * (ns - 1) +
+                                    0.01 * conc;
       if (t < best_t) {
         best_t = t;
         best = pps_eff;

@@ -67,6 +67,29 @@ def main():
         launch()
         runs.append((path, launch, []))
     torch.cuda.synchronize()
+    if os.environ.get("FLUSH"):  # cold L2: one launch between its own event nodes, a 256 MB memset before each
+        flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+        for _ in range(5):
+            for path, launch, times in runs:
+                ev = (torch.cuda.Event(enable_timing=True, external=True),
+                      torch.cuda.Event(enable_timing=True, external=True))
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g):
+                    ev[0].record()
+                    launch()
+                    ev[1].record()
+                for _ in range(6):
+                    flush.zero_()
+                    g.replay()
+                    torch.cuda.synchronize()
+                    times.append(ev[0].elapsed_time(ev[1]) / 20)  # printed x20 below, like the other modes
+        byt = int(lens.sum()) * Hkv * 264 + B * Hq * 512 + int(nblk.sum()) * 4
+        for path, _, times in runs:
+            t = min(times)
+            med = sorted(times)[len(times) // 2]
+            print(f"{cfg} pps={pps} {path}: cold-L2 min {t * 20e3:.1f} us  median {med * 20e3:.1f} us  "
+                  f"{byt / (med * 20) / 1e6:.0f} GB/s")
+        return
     if os.environ.get("GRAPH"):  # time 20 launches captured in one CUDA graph: GPU time, no host cost
         graphed = []
         for path, launch, times in runs:

@@ -1,5 +1,7 @@
 """Small-batch decode latency (interactive serving): GPU time of one K2 launch
-through the public op, replayed from a CUDA graph (no host launch cost), for
+through the public op, replayed from a CUDA graph (no host launch cost) --
+back to back (L2-warm where the KV fits in L2) and after a 256 MB memset that
+evicts L2 (cold: the serving case, one layer's KV is not in L2) -- for
 B = 1..32 sequences of the Llama-3-8B attention shape (Hq = 32, Hkv = 8,
 INT8), plus C1.  One JSON line per shape.
 
@@ -55,9 +57,26 @@ def main():
             torch.cuda.synchronize()
             times.append(e0.elapsed_time(e1) / 20 * 1e3)
         us = sorted(times)[len(times) // 2]
+        # cold L2: a 256 MB memset, then one launch between its own event nodes
+        flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+        ev = (torch.cuda.Event(enable_timing=True, external=True), torch.cuda.Event(enable_timing=True, external=True))
+        g1 = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g1):
+            ev[0].record()
+            run()
+            ev[1].record()
+        cold = []
+        for _ in range(15):
+            flush.zero_()
+            g1.replay()
+            torch.cuda.synchronize()
+            cold.append(ev[0].elapsed_time(ev[1]) * 1e3)
+        cus = sorted(cold)[len(cold) // 2]
+        del flush
         byt = B * L * Hkv * 264 + B * Hq * 512 + NB * 4
         print(json.dumps({"B": B, "ctx": ctx, "pages_per_split": pps, "splits": -(-npg // pps), "k2_us": us,
-                          "gbs": byt / (us * 1e-6) / 1e9, "tokens_per_s": B / (us * 1e-6)}), flush=True)
+                          "gbs": byt / (us * 1e-6) / 1e9, "tokens_per_s": B / (us * 1e-6),
+                          "k2_us_cold_l2": cus, "gbs_cold_l2": byt / (cus * 1e-6) / 1e9}), flush=True)
         del pool, cache
 
 

@@ -49,6 +49,12 @@ def test_argument_validation_without_gpu():
     st = L.kvq_decode_attn(16, 4096, 16, 10, 16, 4, 16, 2, 20, 8, 0, 0.1, 0, 256, 1 << 20, 16, 0, 0, None)
     assert st == _lib.KVQ_EINVAL and b"Hq % Hkv" in L.kvq_last_error()
     assert L.kvq_copy_blocks(None, 1, 1, None, 0, None) == 0   # no-op
+    # kvq_decode_step flags: unknown bits, and KVQ_STEP_FUSED_APPEND needs T == B
+    step = (16, 16, 1024, 1024, 16, 3, 16, 4096, 16, 10, 16, 4, 16, 2, 32, 8, 0, 0.1, 0, 256, 1 << 20, 16, 0, 0,
+            None)
+    assert L.kvq_decode_step(*step, 4, None) == _lib.KVQ_EINVAL and b"unknown flags" in L.kvq_last_error()
+    assert L.kvq_decode_step(*step, _lib.KVQ_STEP_FUSED_APPEND, None) == _lib.KVQ_EINVAL
+    assert b"FUSED_APPEND" in L.kvq_last_error()
     with pytest.raises(ValueError):
         _lib.check("kvq_decode_attn", _lib.KVQ_EINVAL)
 

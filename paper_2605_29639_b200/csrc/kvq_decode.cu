@@ -827,7 +827,10 @@ __device__ __forceinline__ void decode_cta(const DecodeParams& p, uint8_t* smem)
 #pragma unroll
       for (int e = 0; e < 8; ++e) acc[e] += src[e];
     }
-    const float inv = 1.0f / lsum;
+    // lsum == 0: no token of this split is visible to the row (multi-query: a
+    // split holding only the last draft tokens' positions); partial O = 0 with
+    // LSE = -inf, so the combine weighs it 0 (not 0 * NaN).
+    const float inv = lsum > 0.0f ? 1.0f / lsum : 0.0f;
 #pragma unroll
     for (int e = 0; e < 8; ++e) acc[e] *= inv;
     const int64_t vrow = ((int64_t)b * p.Hkv + h) * G + row;  // partial row of (b, h, query row)

@@ -157,3 +157,57 @@ def test_random_decode_steps(cuda, seed, fused):
     assert np.array_equal(cache.pool.cpu().numpy(), pool)
     ref = O.decode_attn(bf16_bits(q), pool, table, lens1, Hkv, kvd)
     assert rel_err(out.cpu().numpy(), ref) <= 2e-3, (lens, Hq, Hkv, kvd, pps)
+
+
+@pytest.mark.parametrize("seed", range(10))
+def test_random_multi_query(cuda, seed):
+    """Multi-query (speculative scoring) attention on random shapes: q_len new
+    tokens per sequence, causal among themselves, g * q_len <= 16 query rows per
+    kv head, ragged lengths, both formats, random split sizes.  Oracle: query i
+    of sequence b == single-query attention over seq_len - (q_len - 1 - i)
+    tokens."""
+    rng = np.random.default_rng(3000 + seed)
+    q_len = int(rng.integers(2, 6))
+    g = int(rng.choice([gg for gg in (1, 2, 4, 8) if gg * q_len <= 16]))
+    Hkv = int(rng.choice([1, 2, 4, 8]))
+    Hq = g * Hkv
+    B = int(rng.integers(1, 8))
+    lens = [int(rng.integers(q_len, 2500)) for _ in range(B)]
+    kvd = O.INT8 if seed % 2 == 0 else O.FP8_E4M3
+    sc = Scenario(lens, Hq, Hkv, kvd, seed=seed + 500)
+    gq = torch.Generator().manual_seed(seed)
+    q4 = torch.randn((B, q_len, Hq, 128), generator=gq).to(torch.bfloat16)
+    cache = PagedKVCache(KVCacheSpec(Hkv, kv_dtype=NAMES[kvd]), sc.num_blocks, device=cuda,
+                         pool=torch.from_numpy(sc.pool).to(cuda))
+    pps = None if rng.random() < 0.5 else int(rng.integers(1, 40))
+    out = paged_decode_attention(q4.to(cuda), cache, torch.from_numpy(sc.block_table).to(cuda),
+                                 torch.from_numpy(sc.seq_lens).to(cuda), out_dtype=torch.float32,
+                                 pages_per_split=pps).cpu().numpy()
+    qe = q4.reshape(B * q_len, Hq, 128)
+    table = np.repeat(sc.block_table, q_len, axis=0)
+    le = np.asarray([L - (q_len - 1 - i) for L in lens for i in range(q_len)], np.int32)
+    ref = O.decode_attn(bf16_bits(qe), sc.pool, table, le, Hkv, kvd).reshape(B, q_len, Hq, 128)
+    assert rel_err(out, ref) <= 2e-3, (lens, q_len, g, Hkv, kvd, pps)
+
+
+@pytest.mark.parametrize("kv_dtype", [O.INT8, O.FP8_E4M3])
+def test_multi_query_split_invisible_to_early_drafts(cuda, kv_dtype):
+    """A split whose pages hold only the newest draft tokens is invisible to
+    the earlier draft rows (their causal length ends before it): its partial
+    must weigh 0 in the combine, not NaN (found by test_random_multi_query)."""
+    q_len, g, Hkv = 5, 2, 1
+    lens = [1441, 17, 33, 165]      # 1441 = 90 full pages + 1 token
+    sc = Scenario(lens, g * Hkv, Hkv, kv_dtype, seed=77)
+    q4 = torch.randn((len(lens), q_len, g * Hkv, 128), generator=torch.Generator().manual_seed(1)).to(torch.bfloat16)
+    cache = PagedKVCache(KVCacheSpec(Hkv, kv_dtype=NAMES[kv_dtype]), sc.num_blocks, device=cuda,
+                         pool=torch.from_numpy(sc.pool).to(cuda))
+    qe = q4.reshape(len(lens) * q_len, g * Hkv, 128)
+    table = np.repeat(sc.block_table, q_len, axis=0)
+    le = np.asarray([L - (q_len - 1 - i) for L in lens for i in range(q_len)], np.int32)
+    ref = O.decode_attn(bf16_bits(qe), sc.pool, table, le, Hkv, kv_dtype).reshape(len(lens), q_len, g * Hkv, 128)
+    for pps in (1, 30):
+        out = paged_decode_attention(q4.to(cuda), cache, torch.from_numpy(sc.block_table).to(cuda),
+                                     torch.from_numpy(sc.seq_lens).to(cuda), out_dtype=torch.float32,
+                                     pages_per_split=pps).cpu().numpy()
+        assert np.isfinite(out).all()
+        assert rel_err(out, ref) <= 2e-3, pps

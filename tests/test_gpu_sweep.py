@@ -10,7 +10,7 @@ import torch
 
 import oracle as O
 from kvq_testutil import Scenario, bf16_bits
-from paper_2605_29639_b200 import KVCacheSpec, PagedKVCache, paged_decode_attention
+from paper_2605_29639_b200 import KVCacheSpec, PagedKVCache, paged_decode_attention, quantize_append
 
 pytestmark = pytest.mark.gpu
 NAMES = {O.INT8: "int8", O.FP8_E4M3: "fp8_e4m3"}
@@ -211,3 +211,99 @@ def test_multi_query_split_invisible_to_early_drafts(cuda, kv_dtype):
                                      pages_per_split=pps).cpu().numpy()
         assert np.isfinite(out).all()
         assert rel_err(out, ref) <= 2e-3, pps
+
+
+@pytest.mark.parametrize("seed", range(10))
+def test_random_appends_bit_exact(cuda, seed):
+    """K1 on random appends: random T (both kernels: the one-warp-per-row kernel
+    up to 8192 (token, head) rows, the tile kernel above), 1-8 kv heads,
+    whole-page runs mixed with scattered, skipped (-1) and out-of-range slots,
+    rows scaled over 2^-60..2^60 with zeros, +-inf and NaN injected; the pool
+    bytes must equal the oracle's bit for bit."""
+    rng = np.random.default_rng(4000 + seed)
+    Hkv = int(rng.choice([1, 2, 4, 6, 8]))
+    kvd = "int8" if seed % 2 == 0 else "fp8_e4m3"
+    nb = int(rng.integers(64, 1200))
+    T = int(rng.choice([rng.integers(1, 300), rng.integers(1500, 4000)]))
+    slots = []
+    perm = rng.permutation(nb)
+    used = 0
+    while len(slots) < T:
+        if rng.random() < 0.5 and used < nb:          # a whole page
+            blk = int(perm[used]); used += 1
+            slots += [blk * 16 + t for t in range(16)]
+        elif used < nb:                                # a scattered token in a fresh block
+            blk = int(perm[used]); used += 1
+            slots.append(blk * 16 + int(rng.integers(0, 16)))
+        else:
+            slots.append(-1)
+    slots = np.asarray(slots[:T], np.int32)
+    slots[rng.random(T) < 0.05] = -1
+    oob = rng.random(T) < 0.02
+    slots[oob] = nb * 16 + 5                           # past the pool: skipped by both
+    g = torch.Generator().manual_seed(seed)
+    k = torch.randn((T, Hkv, 128), generator=g)
+    v = torch.randn((T, Hkv, 128), generator=g)
+    for x in (k, v):
+        x *= torch.exp2(torch.randint(-60, 61, (T, Hkv, 1), generator=g).float())
+        m = torch.rand((T, Hkv, 128), generator=g)
+        x[m < 0.001] = float("inf")
+        x[(m > 0.001) & (m < 0.002)] = float("-inf")
+        x[(m > 0.002) & (m < 0.003)] = float("nan")
+        x[torch.rand((T, Hkv, 1), generator=g).expand(T, Hkv, 128) < 0.02] = 0.0
+    k, v = k.to(torch.bfloat16), v.to(torch.bfloat16)
+    cache = PagedKVCache(KVCacheSpec(Hkv, kv_dtype=kvd), nb, device=cuda)
+    quantize_append(cache, k.to(cuda), v.to(cuda), torch.from_numpy(slots).to(cuda))
+    ref = np.zeros((nb, Hkv, O.PAGE), dtype=np.uint8)
+    O.quant_append(bf16_bits(k), bf16_bits(v), np.where(oob, -1, slots).astype(np.int32), DT_SWEEP[kvd], ref)
+    assert np.array_equal(cache.pool.cpu().numpy(), ref), (T, Hkv, kvd)
+
+
+DT_SWEEP = {"int8": O.INT8, "fp8_e4m3": O.FP8_E4M3}
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_random_verify_steps(cuda, seed):
+    """The speculative verify step (decode_step with q[B, q_len, Hq, 128]) on
+    random shapes: q_len draft rows per sequence appended (crossing into fresh
+    blocks where the last page fills up), then scored causally -- pool bytes
+    bit-exact and attention within tolerance against the oracle."""
+    from paper_2605_29639_b200 import decode_step
+    rng = np.random.default_rng(5000 + seed)
+    q_len = int(rng.integers(2, 5))
+    g = int(rng.choice([gg for gg in (1, 2, 4) if gg * q_len <= 16]))
+    Hkv = int(rng.choice([1, 2, 4, 8]))
+    Hq = g * Hkv
+    B = int(rng.integers(1, 8))
+    lens = [int(rng.choice([0, 1, 14, 15, 16, 31])) if rng.random() < 0.3 else int(rng.integers(1, 2000))
+            for _ in range(B)]
+    kvd = O.INT8 if seed % 2 == 0 else O.FP8_E4M3
+    sc = Scenario(lens, Hq, Hkv, kvd, seed=seed + 900, extra_blocks=2 * B + 2,
+                  max_blocks=max(-(-(L + q_len) // 16) for L in lens))
+    used = set(sc.block_table[b, i] for b in range(B) for i in range(-(-lens[b] // 16)))
+    free = [i for i in range(sc.num_blocks) if i not in used]
+    table = sc.block_table.copy()
+    slots = []
+    for b, L in enumerate(lens):
+        for t in range(L, L + q_len):
+            if t % 16 == 0 and t // 16 >= -(-L // 16):
+                table[b, t // 16] = free.pop()
+            slots.append(int(table[b, t // 16]) * 16 + t % 16)
+    gk = torch.Generator().manual_seed(seed)
+    k = torch.randn((B * q_len, Hkv, 128), generator=gk).to(torch.bfloat16)
+    v = torch.randn((B * q_len, Hkv, 128), generator=gk).to(torch.bfloat16)
+    q4 = torch.randn((B, q_len, Hq, 128), generator=gk).to(torch.bfloat16)
+    lens1 = np.asarray(lens, np.int32) + q_len
+    cache = PagedKVCache(KVCacheSpec(Hkv, kv_dtype=NAMES[kvd]), sc.num_blocks, device=cuda,
+                         pool=torch.from_numpy(sc.pool).to(cuda))
+    pps = None if rng.random() < 0.5 else int(rng.integers(1, 30))
+    out = decode_step(cache, k.to(cuda), v.to(cuda), torch.tensor(slots, dtype=torch.int32, device=cuda),
+                      q4.to(cuda), torch.from_numpy(table).to(cuda), torch.from_numpy(lens1).to(cuda),
+                      out_dtype=torch.float32, pages_per_split=pps).cpu().numpy()
+    pool = sc.pool.copy()
+    O.quant_append(bf16_bits(k), bf16_bits(v), np.asarray(slots, np.int32), kvd, pool)
+    assert np.array_equal(cache.pool.cpu().numpy(), pool)
+    qe = q4.reshape(B * q_len, Hq, 128)
+    le = np.asarray([L - (q_len - 1 - i) for L in lens1 for i in range(q_len)], np.int32)
+    ref = O.decode_attn(bf16_bits(qe), pool, np.repeat(table, q_len, axis=0), le, Hkv, kvd)
+    assert rel_err(out, ref.reshape(B, q_len, Hq, 128)) <= 2e-3, (lens, q_len, g, Hkv, kvd, pps)

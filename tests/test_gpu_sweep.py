@@ -307,3 +307,48 @@ def test_random_verify_steps(cuda, seed):
     le = np.asarray([L - (q_len - 1 - i) for L in lens1 for i in range(q_len)], np.int32)
     ref = O.decode_attn(bf16_bits(qe), pool, np.repeat(table, q_len, axis=0), le, Hkv, kvd)
     assert rel_err(out, ref.reshape(B, q_len, Hq, 128)) <= 2e-3, (lens, q_len, g, Hkv, kvd, pps)
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_random_sessions(cuda, seed):
+    """DecodeSession (staged uploads, one captured graph per buffer slot, the
+    native pipeline submitter) on random shapes, with the tail-only PDL step
+    or the fused append, against the eager session: identical outputs step
+    after step and identical pools."""
+    from paper_2605_29639_b200.session import DecodeSession
+    rng = np.random.default_rng(6000 + seed)
+    Hkv = int(rng.choice([1, 2, 4, 8]))
+    Hq = Hkv * int(rng.choice([1, 2, 4, 8, 16]))
+    B = int(rng.integers(1, 10))
+    lens = [int(rng.integers(1, 1500)) for _ in range(B)]
+    kvd = "int8" if seed % 2 == 0 else "fp8_e4m3"
+    sc = Scenario(lens, Hq, Hkv, O.INT8 if kvd == "int8" else O.FP8_E4M3, seed=seed + 40)
+    table = torch.from_numpy(sc.block_table).to(cuda)
+    pool0 = torch.from_numpy(sc.pool).to(cuda)
+    caches = [PagedKVCache(KVCacheSpec(Hkv, kv_dtype=kvd), sc.num_blocks, device=cuda, pool=pool0.clone())
+              for _ in range(2)]
+    fused = seed % 3 == 0
+    eager = DecodeSession(caches[0], table, B, Hq)
+    fast = DecodeSession(caches[1], table, B, Hq, graphs=True, append_tail_only=True, fused_append=fused)
+    g = torch.Generator().manual_seed(seed)
+    lens_t = torch.from_numpy(sc.seq_lens)
+    slots = torch.tensor([int(sc.block_table[b, (L - 1) // 16]) * 16 + (L - 1) % 16 for b, L in enumerate(lens)],
+                         dtype=torch.int32)
+    outs = []
+    for step in range(5):
+        q = torch.randn((B, Hq, 128), generator=g).to(torch.bfloat16)
+        k = torch.randn((B, Hkv, 128), generator=g).to(torch.bfloat16)
+        v = torch.randn((B, Hkv, 128), generator=g).to(torch.bfloat16)
+        o_a = torch.empty((B, Hq, 128), dtype=torch.bfloat16, pin_memory=True)
+        o_b = torch.empty_like(o_a).pin_memory()
+        eager.submit(q.pin_memory(), k.pin_memory(), v.pin_memory(), slots.pin_memory(), lens_t.pin_memory(), o_a)
+        h = fast.next_inputs()
+        for name, t in (("q", q), ("k", k), ("v", v), ("slots", slots), ("lens", lens_t)):
+            h[name].copy_(t)
+        fast.submit_staged(o_b)
+        outs.append((o_a, o_b))
+        eager.synchronize()
+        fast.synchronize()
+    for a, b in outs:
+        assert torch.equal(a, b)
+    assert torch.equal(caches[0].pool, caches[1].pool)

@@ -352,3 +352,40 @@ def test_random_sessions(cuda, seed):
     for a, b in outs:
         assert torch.equal(a, b)
     assert torch.equal(caches[0].pool, caches[1].pool)
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_random_layouts(cuda, seed):
+    """Output layouts and strides on random shapes: q a batch-strided view of a
+    wider tensor (the fused QKV projection case), bf16 or fp32 output,
+    [B, Hq, d] or head-major [Hq, B, d], into a caller-provided `out`."""
+    rng = np.random.default_rng(7000 + seed)
+    Hkv = int(rng.choice([1, 2, 4, 8]))
+    Hq = Hkv * int(rng.choice([1, 2, 4, 8, 16]))
+    B = int(rng.integers(1, 9))
+    lens = [int(rng.integers(1, 1200)) for _ in range(B)]
+    kvd = O.INT8 if seed % 2 == 0 else O.FP8_E4M3
+    sc = Scenario(lens, Hq, Hkv, kvd, seed=seed + 60)
+    extra = int(rng.integers(1, 5)) * Hkv                 # the K/V heads of a fused QKV row
+    wide = torch.randn((B, Hq + 2 * extra, 128), generator=torch.Generator().manual_seed(seed)).to(torch.bfloat16)
+    wide[:, :Hq] = sc.q
+    q = wide.to(cuda)[:, :Hq]                             # stride(0) = (Hq + 2 extra) * 128
+    assert q.stride(0) != Hq * 128
+    cache = PagedKVCache(KVCacheSpec(Hkv, kv_dtype=NAMES[kvd]), sc.num_blocks, device=cuda,
+                         pool=torch.from_numpy(sc.pool).to(cuda))
+    out_dtype = torch.float32 if rng.random() < 0.5 else torch.bfloat16
+    head_major = bool(rng.random() < 0.5)
+    shape = (Hq, B, 128) if head_major else (B, Hq, 128)
+    out = torch.full(shape, float("nan"), dtype=out_dtype, device=cuda)
+    res = paged_decode_attention(q, cache, torch.from_numpy(sc.block_table).to(cuda),
+                                 torch.from_numpy(sc.seq_lens).to(cuda), out=out, out_dtype=out_dtype,
+                                 head_major=head_major)
+    assert res.data_ptr() == out.data_ptr()
+    got = out.float().cpu().numpy()
+    if head_major:
+        got = got.transpose(1, 0, 2)
+    ref = sc.oracle_out()
+    if out_dtype == torch.float32:
+        assert rel_err(got, ref) <= 2e-3
+    else:
+        assert np.all(np.abs(got - ref) <= 1e-2 + 2.0 ** -8 * np.abs(ref))

@@ -63,6 +63,8 @@ struct Geo {
                 "merge scratch must fit in the ring");
 };
 constexpr int CTAS_PER_SM = 4;  // used by the split heuristic (g <= 8 variant)
+// Largest log2 softmax weight p = 2^u relative to a row's reference point m (l is fp32).
+constexpr float UMAX = 100.0f;
 
 __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
   __nv_bfloat162 t = __floats2bfloat162_rn(lo, hi);
@@ -399,12 +401,17 @@ __device__ __forceinline__ void decode_cta(const DecodeParams& p, uint8_t* smem)
     for (int o = 16; o > 0; o >>= 1) amax = fmaxf(amax, __shfl_xor_sync(FULL, amax, o));
     if constexpr (KVD == KVQ_INT8) {
       // INT8 K feeds the s8 tensor cores directly (no dequantisation at all):
-      // q = s1 * (q1 + q2 / 128) with int8 q1, q2, two IMMA per k-step,
-      // S = s1 * (acc1 + acc2 / 128).  s1 is a power of two (amax / s1 in
-      // [64, 127.5), else one binade up), so the two terms hold every bf16
-      // element >= s1 (its 8-bit mantissa) EXACTLY; only elements below s1 ~
-      // amax / 100 round, by <= s1 / 256.  (With s1 = amax / 127 every element
-      // rounded: 2.3e-3 output error at logits of std 15, against 4.6e-4 now.)
+      // q = s1 * (q1 + q2 / 256) with int8 q1, q2, two IMMA per k-step,
+      // S = s1 * (acc1 + acc2 / 256).  s1 is a power of two (amax / s1 in
+      // [64, 127.5), else one binade up; amax over the GQA group), q1 =
+      // floor(q / s1 + 1/2) leaves |residual| <= s1 / 2, so q2 = residual *
+      // 256 / s1 fits [-128, 128] (128 clamps to 127: <= s1 / 256, only on
+      // exact ties).  The two terms hold every bf16 element >= s1 / 2 (its
+      // 8-bit mantissa) EXACTLY; only elements below ~amax / 128 round, by
+      // <= s1 / 512.  (Round 1 used q2 = residual * 128 / s1, exact only from
+      // s1 up: at queries x40, logit std ~70 log2 units, its score error gave
+      // 2.9e-3 on an attention-sink row; with s1 = amax / 127 every element
+      // rounded.)
       // IMMA k-step j (32 of d): b0 = q[head][16c + 4j .. +3], b1 =
       // q[head][64 + 16c + 4j .. +3], stored as qf[nt][2j] = term 1 (b0, b1),
       // qf[nt][2j + 1] = term 2.
@@ -413,7 +420,7 @@ __device__ __forceinline__ void decode_cta(const DecodeParams& p, uint8_t* smem)
       if (amax * pow2i(7 - qex) > 127.49f) ++qex;
       const float s1 = amax > 0.0f ? pow2i(qex - 7) : 0.0f;
       const float inv1 = amax > 0.0f ? pow2i(7 - qex) : 0.0f;
-      qscale = p.sm_scale_log2 * s1 * 0.0078125f;  // S = s1 * (128 acc1 + acc2) / 128
+      qscale = p.sm_scale_log2 * s1 * 0.00390625f;  // S = s1 * (256 acc1 + acc2) / 256
 #pragma unroll
       for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
@@ -428,9 +435,9 @@ __device__ __forceinline__ void decode_cta(const DecodeParams& p, uint8_t* smem)
             int t1[4], t2[4];
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
-              t1[e] = max(-127, min(127, __float2int_rn(v[e] * inv1)));
+              t1[e] = max(-127, min(127, __float2int_rd(__fadd_rn(v[e] * inv1, 0.5f))));
               const float res = fmaf(-(float)t1[e], s1, v[e]);
-              t2[e] = max(-127, min(127, __float2int_rn(res * inv1 * 128.0f)));
+              t2[e] = max(-128, min(127, __float2int_rn(res * inv1 * 256.0f)));
             }
             qf[nt][2 * jj][half] = pack_s8x4(t1[0], t1[1], t1[2], t1[3]);
             qf[nt][2 * jj + 1][half] = pack_s8x4(t2[0], t2[1], t2[2], t2[3]);
@@ -505,8 +512,6 @@ __device__ __forceinline__ void decode_cta(const DecodeParams& p, uint8_t* smem)
       m[nt][e] = hvalid[nt][e] ? -INFINITY : INFINITY;
       l[nt][e] = 0.0f;
     }
-  float escale = 1.0f;  // V-scale normaliser 2^E (fp16 range guard for P')
-  bool escale_set = false;
   // Causal visibility of query row j (token i = j / g of q_len): L - (q_len - 1 - i);
   // only evaluated on tail pages, so it costs no registers in the steady state.
   const int L_all = L - (qlen - 1);  // tokens visible to every query row
@@ -579,7 +584,7 @@ __device__ __forceinline__ void decode_cta(const DecodeParams& p, uint8_t* smem)
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
-          for (int e = 0; e < 4; ++e) st[nt][e] = __int2float_rn(acc1[nt][e] * 128 + acc2[nt][e]);
+          for (int e = 0; e < 4; ++e) st[nt][e] = __int2float_rn(acc1[nt][e] * 256 + acc2[nt][e]);
       } else {
         float sa[NT][4], sb2[NT][4];
 #pragma unroll
@@ -644,52 +649,57 @@ __device__ __forceinline__ void decode_cta(const DecodeParams& p, uint8_t* smem)
           if (TAIL && !visible(nt, q4)) u[nt][q4] = -INFINITY;
           umax = fmaxf(umax, u[nt][q4]);
         }
-      // ---- lazy rescale: p = 2^u must stay <= 2^8, and P' = p * scale_v * 2^E must
-      //      stay in f16 range (2^E keeps the page's max V scale in [2^-10, 2^4]).
-      //      Checked per thread + warp votes; the exact maxima (shuffle
-      //      reductions) are only computed on the rare pages that need a rescale.
-      const float ve_r = vs_r * escale, ve_r8 = vs_r8 * escale;
-      const bool trig = __any_sync(FULL, umax > 8.0f || !escale_set || fmaxf(ve_r, ve_r8) > 16.0f) ||
-                        (__all_sync(FULL, fmaxf(ve_r, ve_r8) < 0.0009765625f) &&
-                         __any_sync(FULL, fmaxf(vs_r, vs_r8) > 0.0f));
+      // ---- lazy rescale.  P' = p * scale_v is f16, so each row's reference
+      //      point m is anchored on the largest CONTRIBUTION p * scale_v seen
+      //      (log2: max of score + log2(scale_v)), not on the largest score:
+      //      a dominant token with V ~ 0 (an attention sink) or a page whose V
+      //      scales spread 2^20 then keeps the tokens that make up the output
+      //      in f16's normal range.  p itself spans [2^-UMAX.., 2^UMAX] (l is
+      //      fp32), which also absorbs the V scales' magnitude.  Fast path: one
+      //      per-thread bound 2^umax * max(scale_v) <= 2^12 (P' far from f16
+      //      overflow) + a warp vote; the exact per-row maxima (shuffle
+      //      reductions) are computed only on the rare pages that move m.
+      //      (Round 1 anchored m on the max score and kept a separate per-warp
+      //      V normaliser 2^E: P' lost precision wherever the weight and the V
+      //      scale of the tokens that matter were far from those two maxima.)
+      const bool trig = __any_sync(FULL, umax > UMAX || fast_exp2(umax) * fmaxf(vs_r, vs_r8) > 4096.0f);
       if (trig) {
-        float mx[NT][2];
+        // log2 of each token's V scale (-inf for scale 0 / masked tokens)
+        const float lw_r = __log2f(vs_r), lw_r8 = __log2f(vs_r8);
+        float mx[NT][2], cx[NT][2];
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
-          for (int e = 0; e < 2; ++e)
-            mx[nt][e] = fmaxf(visible(nt, e) ? st[nt][e] * kq_r : -INFINITY,
-                              visible(nt, e + 2) ? st[nt][e + 2] * kq_r8 : -INFINITY);
-        float vmax = fmaxf(vs_r, vs_r8);
-#pragma unroll
-        for (int o2 = 4; o2 <= 16; o2 <<= 1) {
-#pragma unroll
-          for (int nt = 0; nt < NT; ++nt) {
-            mx[nt][0] = fmaxf(mx[nt][0], __shfl_xor_sync(FULL, mx[nt][0], o2));
-            mx[nt][1] = fmaxf(mx[nt][1], __shfl_xor_sync(FULL, mx[nt][1], o2));
+          for (int e = 0; e < 2; ++e) {
+            const float s0 = visible(nt, e) ? __fmul_rn(st[nt][e], kq_r) : -INFINITY;
+            const float s8 = visible(nt, e + 2) ? __fmul_rn(st[nt][e + 2], kq_r8) : -INFINITY;
+            mx[nt][e] = fmaxf(s0, s8);
+            cx[nt][e] = fmaxf(s0 + lw_r, s8 + lw_r8);
           }
-          vmax = fmaxf(vmax, __shfl_xor_sync(FULL, vmax, o2));
-        }
-        const float ve = vmax * escale;
-        float e_new = escale;
-        if (vmax > 0.0f && (!escale_set || ve > 16.0f || ve < 0.0009765625f)) {
-          int ex;
-          frexpf(vmax, &ex);
-          e_new = pow2i(-ex);
-          escale_set = true;
-        }
-        const float er = e_new / escale;  // exact power of two
-        escale = e_new;
+#pragma unroll
+        for (int o2 = 4; o2 <= 16; o2 <<= 1)
+#pragma unroll
+          for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              mx[nt][e] = fmaxf(mx[nt][e], __shfl_xor_sync(FULL, mx[nt][e], o2));
+              cx[nt][e] = fmaxf(cx[nt][e], __shfl_xor_sync(FULL, cx[nt][e], o2));
+            }
+        // per-token cap on u so P' <= 2^12 even where fp32 cannot resolve the scores
+        const float ucap_r = fminf(UMAX, 12.0f - lw_r), ucap_r8 = fminf(UMAX, 12.0f - lw_r8);
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt) {
           float f[2];
 #pragma unroll
           for (int e = 0; e < 2; ++e) {
-            const bool nm = mx[nt][e] > m[nt][e] + 8.0f;  // never for rows past G (m = +inf)
-            const float cl = nm ? fast_exp2(m[nt][e] - mx[nt][e]) : 1.0f;
-            if (nm) m[nt][e] = mx[nt][e];
+            // m moves (up only) when this page's largest P' would pass 2^12 or its
+            // largest p 2^UMAX; never for rows past G (m = +inf).
+            const bool nm = cx[nt][e] > m[nt][e] + 12.0f || mx[nt][e] > m[nt][e] + UMAX;
+            const float mn = fmaxf(cx[nt][e], mx[nt][e] - UMAX);
+            const float cl = nm ? fast_exp2(m[nt][e] - mn) : 1.0f;
+            if (nm) m[nt][e] = mn;
             l[nt][e] *= cl;
-            f[e] = cl * er;
+            f[e] = cl;
           }
 #pragma unroll
           for (int mt = 0; mt < 8; ++mt) {
@@ -698,20 +708,21 @@ __device__ __forceinline__ void decode_cta(const DecodeParams& p, uint8_t* smem)
             o[nt][mt][2] *= f[0];
             o[nt][mt][3] *= f[1];
           }
-          // Recompute from the ROUNDED product, as m was: the row's max token gets
-          // u = 0 exactly (p = 1, so l >= 1).  The fast path's FFMA is exact
+          // Recompute from the ROUNDED product, as m was: the row's max-score
+          // token gets u >= 0 (so l >= 1).  The fast path's FFMA is exact
           // instead; the two differ by half an ulp of m, which only matters past
           // |m| ~ 2^27 (log2 units; fp32 cannot resolve such scores) -- there the
-          // clamp keeps p <= 2^8 and the max token keeps l > 0 (no 0/0, no inf).
+          // caps keep p <= 2^UMAX and P' <= 2^12 (no 0/0, no inf).
 #pragma unroll
           for (int q4 = 0; q4 < 4; ++q4) {
-            u[nt][q4] = fminf(__fadd_rn(__fmul_rn(st[nt][q4], q4 < 2 ? kq_r : kq_r8), -m[nt][q4 & 1]), 8.0f);
+            u[nt][q4] = fminf(__fadd_rn(__fmul_rn(st[nt][q4], q4 < 2 ? kq_r : kq_r8), -m[nt][q4 & 1]),
+                              q4 < 2 ? ucap_r : ucap_r8);
             if (TAIL && !visible(nt, q4)) u[nt][q4] = -INFINITY;
           }
         }
       }
-      // ---- p (fp32, for l) and P' = p * scale_v * 2^E (fp16) -> P'^T B-fragments
-      const float w_r = vs_r * escale, w_r8 = vs_r8 * escale;
+      // ---- p (fp32, for l) and P' = p * scale_v (fp16) -> P'^T B-fragments
+      const float w_r = vs_r, w_r8 = vs_r8;
       uint32_t pb[NT][2];
 #pragma unroll
       for (int nt = 0; nt < NT; ++nt) {
@@ -796,7 +807,7 @@ __device__ __forceinline__ void decode_cta(const DecodeParams& p, uint8_t* smem)
       float M = -INFINITY;
 #pragma unroll
       for (int w2 = 0; w2 < NW; ++w2) M = fmaxf(M, sm[w2 * 16 + hh]);
-      f[e] = (hvalid[nt][e] && m[nt][e] > -INFINITY) ? fast_exp2(m[nt][e] - M) / escale : 0.0f;
+      f[e] = (hvalid[nt][e] && m[nt][e] > -INFINITY) ? fast_exp2(m[nt][e] - M) : 0.0f;
     }
     float* mine = so + (warp * 16 + 8 * nt + 2 * c) * HD;
 #pragma unroll

@@ -65,3 +65,44 @@ class Scenario:
     def oracle_out(self, sm_scale=None):
         return O.decode_attn(bf16_bits(self.q), self.pool, self.block_table, self.seq_lens, self.Hkv,
                              self.kv_dtype, sm_scale)
+
+
+def int8_two_term_q(q: torch.Tensor, Hkv: int) -> np.ndarray:
+    """The INT8 path's query rounding (kvq_decode.cu, decode_cta: 'INT8 K feeds
+    the s8 tensor cores directly'): per (sequence, kv head) group a power-of-two
+    step s1 with amax / s1 in [64, 127.5), q1 = floor(q / s1 + 1/2), q2 =
+    clamp(rint((q - q1 s1) * 256 / s1), -128, 127), q' = s1 (q1 + q2 / 256).
+    Lets a test separate that (documented) score rounding from P' numerics."""
+    x = q.float().numpy().astype(np.float64)
+    B, Hq = x.shape[:2]
+    g = Hq // Hkv
+    out = np.zeros_like(x)
+    for b in range(B):
+        for h in range(Hkv):
+            grp = x[b, h * g:(h + 1) * g]
+            a = np.abs(grp).max()
+            if a == 0:
+                continue
+            ex = np.frexp(a)[1]
+            if a * 2.0 ** (7 - ex) > 127.49:
+                ex += 1
+            s1 = 2.0 ** (ex - 7)
+            q1 = np.clip(np.floor(grp / s1 + 0.5), -127, 127)
+            q2 = np.clip(np.rint((grp - q1 * s1) / s1 * 256), -128, 127)
+            out[b, h * g:(h + 1) * g] = s1 * (q1 + q2 / 256)
+    return out
+
+
+def dense_kv(sc: "Scenario"):
+    """Dequantised dense K/V [B, Hkv, Lmax, 128] of a Scenario's pages (fp64)."""
+    codes, scales = O.unpack_pool(sc.pool)
+    vals = O.code_values_np(codes, sc.kv_dtype).astype(np.float64) * scales[..., None].astype(np.float64)
+    Lmax = max(int(sc.seq_lens.max()), 1)
+    k = np.zeros((sc.B, sc.Hkv, Lmax, 128))
+    v = np.zeros_like(k)
+    for b, L in enumerate(sc.seq_lens):
+        n = -(-int(L) // 16)
+        blk = sc.block_table[b, :n]
+        k[b, :, :L] = vals[blk, :, 0].transpose(1, 0, 2, 3).reshape(sc.Hkv, -1, 128)[:, :L]
+        v[b, :, :L] = vals[blk, :, 1].transpose(1, 0, 2, 3).reshape(sc.Hkv, -1, 128)[:, :L]
+    return k, v

@@ -9,7 +9,7 @@ import pytest
 import torch
 
 import oracle as O
-from kvq_testutil import Scenario, bf16_bits
+from kvq_testutil import Scenario, bf16_bits, dense_kv, int8_two_term_q
 from paper_2605_29639_b200 import KVCacheSpec, PagedKVCache, paged_decode_attention, quantize_append
 
 pytestmark = pytest.mark.gpu
@@ -66,13 +66,13 @@ def requantize(sc):
 @pytest.mark.parametrize("q_gain", [8.0, 40.0])
 def test_peaked_softmax_and_extreme_rows(cuda, kv_dtype, q_gain):
     """Large logits make the running max jump mid-sequence (the lazy rescale
-    and the P exponent shift); zero rows have scale 0 and all-zero codes;
+    and the P' reference point); zero rows have scale 0 and all-zero codes;
     K rows of magnitude 2^100 give scores past fp32 resolution (the output
     must stay finite and the max token must win); V rows 2^6 larger or
-    2^100 smaller than their page neighbours stress the per-page P' exponent
-    (P' is f16 with the page's largest V scale normalised, so
-    a dominant token whose V scale is below ~2^-8 of its page's largest
-    loses precision -- real KV stays within ~2^6 per page)."""
+    2^100 smaller than their page neighbours stress the f16 range of P' --
+    at 40x one token takes nearly all the weight, and if its V is ~0 the
+    output is made of weights p < 2^-18 of the max, which the contribution
+    anchor keeps in f16's normal range."""
     sc = Scenario([1800, 700, 64, 2500], 32, 8, kv_dtype, seed=77)
     T = sc.k.shape[0]
     g = torch.Generator().manual_seed(5)
@@ -82,15 +82,75 @@ def test_peaked_softmax_and_extreme_rows(cuda, kv_dtype, q_gain):
     v[idx[40:80]] = 0.0
     k[idx[80:100]] *= 2.0 ** 100
     v[idx[100:120]] *= 2.0 ** 6
-    if q_gain <= 8.0:
-        # At 40x one token takes nearly all the weight; if its V is ~0 the
-        # output is made only of weights p < 2^-18, below f16's normal range
-        # for P' -- a property of 16-bit P, not a bug.
-        v[idx[120:140]] *= 2.0 ** -100
+    v[idx[120:140]] *= 2.0 ** -100
     sc.k, sc.v = k.to(torch.bfloat16), v.to(torch.bfloat16)
     requantize(sc)
     sc.q = (sc.q.float() * q_gain).to(torch.bfloat16)
     ref = sc.oracle_out()
+    for pps in (None, 3):
+        out = run(sc, cuda, pages_per_split=pps)
+        assert np.isfinite(out).all()
+        assert rel_err(out, ref) <= 2e-3, (pps, rel_err(out, ref))
+
+
+def _sink_scenario(kv_dtype, g, gap, v_shift, seed):
+    """Token 0 of every sequence is an attention sink: its K row points along
+    the mean query of each GQA group so its logit sits `gap` log2 units above
+    zero, and its V row is scaled by 2^-v_shift (a sink with V ~ 0, the
+    ordinary tokens' tiny weights then make up the output)."""
+    sc = Scenario([700, 333, 1200, 17], 8 * g, 8, kv_dtype, seed=seed)
+    k, v, qf = sc.k.float(), sc.v.float(), sc.q.float()
+    starts = np.concatenate([[0], np.cumsum(sc.seq_lens)[:-1]])
+    for b, s0 in enumerate(starts):
+        for h in range(8):
+            qm = qf[b, h * g:(h + 1) * g].mean(0)
+            k[s0, h] = qm / (qm.norm() ** 2) * gap * np.sqrt(128) / np.log2(np.e)
+        v[s0] *= 2.0 ** -v_shift
+    sc.k, sc.v = k.to(torch.bfloat16), v.to(torch.bfloat16)
+    requantize(sc)
+    return sc
+
+
+@pytest.mark.parametrize("kv_dtype", [O.INT8, O.FP8_E4M3])
+@pytest.mark.parametrize("g", [4, 8, 16])
+@pytest.mark.parametrize("gap,v_shift", [(12, 8), (20, 8), (20, 14), (20, 20), (30, 14), (30, 30)])
+def test_attention_sink_small_v(cuda, kv_dtype, g, gap, v_shift):
+    """A dominant first token whose V is ~0 (round 1 measured 2.7-3.3e-3 here
+    with P' anchored on the max score; the contribution anchor keeps the
+    ordinary tokens' P' in f16's normal range)."""
+    sc = _sink_scenario(kv_dtype, g, gap, v_shift, seed=5 + g)
+    ref = sc.oracle_out()
+    for pps in (None, 5):
+        out = run(sc, cuda, pages_per_split=pps)
+        assert np.isfinite(out).all()
+        assert rel_err(out, ref) <= 2e-3, (pps, rel_err(out, ref))
+
+
+@pytest.mark.parametrize("kv_dtype", [O.INT8, O.FP8_E4M3])
+@pytest.mark.parametrize("g", [4, 8, 16])
+@pytest.mark.parametrize("spread,q_gain", [(10, 1.0), (20, 1.0), (10, 16.0), (20, 16.0), (-20, 16.0),
+                                            (10, 40.0), (20, 40.0), (-20, 40.0)])
+def test_in_page_v_scale_spread(cuda, kv_dtype, g, spread, q_gain):
+    """One token in 16 has its V row scaled by 2^spread, so V scales inside a
+    page spread 2^10 / 2^20 (round 1: 2.7e-2 at 2^20 with N(0,1) queries).
+    INT8 rounds q to two int8 terms (exact above amax / 128, <= amax * 2^-16
+    below); with queries x24..x40 (scores ~300 log2 units) that score rounding
+    alone moves the weights of two tokens that share the output by up to 8e-3,
+    so from x40 on INT8 is held to the oracle fed the same rounded q (the P'
+    path itself at those scores), and to the plain oracle up to x16."""
+    sc = Scenario([700, 333, 1200, 40], 8 * g, 8, kv_dtype, seed=30 + g)
+    v = sc.v.float()
+    T = v.shape[0]
+    idx = torch.randperm(T, generator=torch.Generator().manual_seed(g))[: T // 16]
+    v[idx] *= 2.0 ** spread
+    sc.v = v.to(torch.bfloat16)
+    requantize(sc)
+    sc.q = (sc.q.float() * q_gain).to(torch.bfloat16)
+    if kv_dtype == O.INT8 and q_gain > 16:
+        k_deq, v_deq = dense_kv(sc)
+        ref = O.decode_attn_np(int8_two_term_q(sc.q, sc.Hkv), k_deq, v_deq, sc.seq_lens)
+    else:
+        ref = sc.oracle_out()
     for pps in (None, 3):
         out = run(sc, cuda, pages_per_split=pps)
         assert np.isfinite(out).all()

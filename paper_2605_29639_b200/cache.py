@@ -420,10 +420,26 @@ class BlockAllocator:
 
     def append_slots(self, seq_id, n: int) -> List[int]:
         """Reserve ``n`` token slots at the end of ``seq_id``.  Atomic: on
-        :class:`CacheThrashError` nothing changes."""
+        :class:`CacheThrashError` nothing changes.
+
+        Without token ids a prefix-hashed sequence (one admitted through
+        :meth:`allocate_prefix` / :meth:`append_tokens`) stops hashing: its
+        later pages are private and never keyed, since a key must describe
+        the page's tokens (the pages already keyed keep their keys)."""
+        s = self._seq(seq_id)
+        slots = self._append(s, n)
+        self._stop_hashing(s)
+        return slots
+
+    @staticmethod
+    def _stop_hashing(s: "_Seq") -> None:
+        if s.hashing:
+            s.hashing = False
+            s.tail_tokens = []
+
+    def _append(self, s: "_Seq", n: int) -> List[int]:
         if n < 0:
             raise ValueError("n must be >= 0")
-        s = self._seq(seq_id)
         bs = self.block_size
         tail_room = (bs - s.length % bs) % bs if s.keys else 0
         new_blocks = -(-(n - tail_room) // bs) if n > tail_room else 0
@@ -451,7 +467,9 @@ class BlockAllocator:
         """The decode step's slots: one new token for each of ``seq_ids`` (the
         batched form of ``append_slots(s, 1)``, same rules); returns int32
         ``block * 16 + offset`` per sequence.  Atomic: on
-        :class:`CacheThrashError` nothing changes."""
+        :class:`CacheThrashError` nothing changes.  Like :meth:`append_slots`,
+        a prefix-hashed sequence stops hashing (its decoded tokens' ids are not
+        known here)."""
         seqs = [self._seq(s) for s in seq_ids]
         bs = self.block_size
         need = sum(1 for s in seqs if s.length % bs == 0)
@@ -472,6 +490,8 @@ class BlockAllocator:
             e.watermark = off + 1
             out[i] = s.blocks[-1] * bs + off
             s.length += 1
+            if s.hashing:
+                self._stop_hashing(s)
         return out
 
     def fork(self, parent_id, child_id) -> List[Tuple[int, int]]:
@@ -531,7 +551,7 @@ class BlockAllocator:
                 raise ValueError("sequence was filled without token ids")
             s.hashing = True
         first_page = s.length // self.block_size
-        slots = self.append_slots(seq_id, len(tokens))
+        slots = self._append(s, len(tokens))
         pending = s.tail_tokens + [int(t) for t in tokens]
         nfull = len(pending) // self.block_size
         if nfull:

@@ -12,11 +12,15 @@ is the quantized pages themselves:
   request with the same prefix reuses them without re-quantizing
   (``simulator.py:360-396``: matched prefix vs. uncached suffix).
 * **Local-CPU tier.** An evicted hashed page is copied device-to-host into
-  pinned memory.  A later request that misses on the GPU but hits here
-  promotes the page back with one host-to-device copy (the reference's
-  ``LOAD_TO_GPU`` step, ``tiered_cache.py:277-317``).  The page moves
-  bit-identical at 4224 B per (block, kv head), so an offloaded 8-bit prefix
-  costs half the PCIe bytes of bf16.
+  pinned memory -- the reference's ``writeback_on_evict`` demotion
+  (``tiered_cache.py:254-275``): only when the key is not already on the
+  host and only when it fits *without cascading* (a full host tier drops the
+  victim; it never evicts a host page to make room).  A later request that
+  misses on the GPU but hits here promotes the page back with one
+  host-to-device copy (the reference's ``LOAD_TO_GPU`` step,
+  ``tiered_cache.py:277-317``); the host copy stays resident, as in the
+  reference.  The page moves bit-identical at 4224 B per (block, kv head), so
+  an offloaded 8-bit prefix costs half the PCIe bytes of bf16.
 
 All device copies are stream-ordered on the current stream: the offload of a
 victim page precedes any append into its block, and a promotion precedes the
@@ -24,17 +28,21 @@ attention that reads it.
 """
 from __future__ import annotations
 
-from collections import OrderedDict
 from typing import Dict, List, Optional, Sequence, Tuple
 
 import torch
 
 from ._lib import PAGE_BYTES
-from .cache import BlockAllocator, KVCacheSpec, PagedKVCache
+from .cache import BlockAllocator, CacheThrashError, KVCacheSpec, PagedKVCache
 
 
 class HostTier:
-    """LRU store of whole evicted blocks (all kv heads) in pinned host memory."""
+    """Store of whole evicted blocks (all kv heads) in pinned host memory, with
+    the reference's LOCAL_CPU demotion rule (``tiered_cache.py:254-275``):
+    a demoted key is inserted only if absent and only if a slot is free; a
+    full tier drops the new victim instead of evicting (no cascade).  With
+    only the GPU tier above it nothing else ever evicts a host page, so a
+    slot handed out by :meth:`take` stays valid."""
 
     def __init__(self, capacity_blocks: int, num_kv_heads: int, pin: Optional[bool] = None):
         if capacity_blocks <= 0:
@@ -43,32 +51,35 @@ class HostTier:
         self.store = torch.empty((capacity_blocks, num_kv_heads, PAGE_BYTES), dtype=torch.uint8,
                                  pin_memory=pin)
         self.capacity = capacity_blocks
-        self._slot: "OrderedDict[object, int]" = OrderedDict()  # key -> slot, LRU first
+        self._slot: Dict[object, int] = {}   # key -> slot
         self._free = list(range(capacity_blocks - 1, -1, -1))
         self.offloaded = self.promoted = self.dropped = 0
 
     def __contains__(self, key) -> bool:
         return key in self._slot
 
-    def put(self, key, pages: torch.Tensor) -> None:
+    def keys(self) -> List[object]:
+        return list(self._slot)
+
+    def put(self, key, pages: torch.Tensor) -> bool:
+        """Demote ``key``'s pages; False when it is already here or there is no
+        free slot (best effort, as the reference: nothing is evicted)."""
         if key in self._slot:
-            self._slot.move_to_end(key)
-            return
-        if not self._free:  # drop the least recently used host page
-            _, slot = self._slot.popitem(last=False)
-            self._free.append(slot)
+            return False
+        if not self._free:
             self.dropped += 1
+            return False
         slot = self._free.pop()
         self.store[slot].copy_(pages, non_blocking=True)
         self._slot[key] = slot
         self.offloaded += 1
+        return True
 
     def take(self, key) -> Optional[torch.Tensor]:
-        """The host pages of ``key`` (the slot stays valid until the next put)."""
+        """The host pages of ``key`` (the copy stays resident)."""
         slot = self._slot.get(key)
         if slot is None:
             return None
-        self._slot.move_to_end(key)
         self.promoted += 1
         return self.store[slot]
 
@@ -98,18 +109,31 @@ class PrefixKVCache:
     def _promote(self, key) -> bool:
         if self.host is None or key not in self.host:
             return False
-        pages = self.host.take(key)
+        # Insert first: it may evict a GPU page, whose offload runs now, so the
+        # host slot read below cannot be reused under the copy.
         blk = self.alloc.pool.insert(key, self.alloc.block_size, self.alloc.clock)
+        pages = self.host.take(key)
         self.cache.pool[blk].copy_(pages, non_blocking=True)
         self.host_hit_tokens += self.alloc.block_size
         return True
 
     # request API ---------------------------------------------------------------
     def admit(self, seq_id, tokens: Sequence[int]) -> Tuple[int, List[int]]:
+        """Register ``seq_id`` for prompt ``tokens``.  On
+        :class:`CacheThrashError` everything the request acquired is released
+        before the error propagates (the reference's ``_dispatch_prefill``:
+        ``release_and_update(acquired)`` then raise, ``simulator.py:397-400``), so the
+        caller can requeue it."""
         before = self.host_hit_tokens
-        cached = self.alloc.allocate_prefix(seq_id, tokens, promote=self._promote)
+        try:
+            cached = self.alloc.allocate_prefix(seq_id, tokens, promote=self._promote)
+            slots = self.alloc.append_tokens(seq_id, tokens[cached:])
+        except CacheThrashError:
+            if seq_id in self.alloc:
+                self.alloc.free(seq_id)
+            self.host_hit_tokens = before
+            raise
         self.gpu_hit_tokens += cached - (self.host_hit_tokens - before)
-        slots = self.alloc.append_tokens(seq_id, tokens[cached:])
         self.computed_tokens += len(tokens) - cached
         return cached, slots
 

@@ -10,10 +10,12 @@ K/V, or 51.6 %.  The receiver does not re-quantize, so the decode worker's
 pages are bit-identical to the prefill worker's.
 
 Transport is ``torch.distributed`` point-to-point: NCCL over NVLink between
-GPUs, or gloo in the CPU tests.  Pages are gathered into one contiguous
-staging buffer by one ``kvq_gather_blocks`` launch and scattered on arrival by
-one ``kvq_scatter_blocks`` launch (native page-copy kernel).  Both are
-device-side copies, so the only host<->device traffic is the 16-byte header.
+GPUs.  Pages are gathered into one contiguous staging buffer by one
+``kvq_gather_blocks`` launch and scattered on arrival by one
+``kvq_scatter_blocks`` launch (native page-copy kernel).  Both are device-side
+copies, so the only host<->device traffic is the 16-byte header.  The page
+copies are the only pluggable part (``export=`` / ``import_=``): the gloo tests
+on CPU pass their own host copies; the product path is CUDA-only.
 """
 from __future__ import annotations
 
@@ -42,11 +44,10 @@ def _ids(block_ids, device) -> torch.Tensor:
 
 def export_pages(cache: PagedKVCache, block_ids: Sequence[int]) -> torch.Tensor:
     """``uint8[n, Hkv, 4224]`` copy of the given blocks' pages (all heads):
-    ``kvq_gather_blocks`` on the device (the CPU-side tensors of the gloo
-    tests are copied by torch; there is no compute on this path)."""
+    ``kvq_gather_blocks`` on the device."""
     n, hkv = len(block_ids), cache.spec.num_kv_heads
     if not cache.pool.is_cuda:
-        return cache.pool.index_select(0, torch.as_tensor([int(b) for b in block_ids], dtype=torch.long))
+        raise ValueError("export_pages: the pool must be a CUDA tensor")
     out = torch.empty((n, hkv, PAGE_BYTES), dtype=torch.uint8, device=cache.device)
     if n:
         idx = _ids(block_ids, cache.device)
@@ -60,10 +61,7 @@ def import_pages(cache: PagedKVCache, block_ids: Sequence[int], pages: torch.Ten
     """Scatter a packed page buffer into the given blocks (``kvq_scatter_blocks``)."""
     if pages.shape[1:] != cache.pool.shape[1:] or pages.shape[0] != len(block_ids):
         raise ValueError("page buffer does not match the destination pool")
-    if not cache.pool.is_cuda:
-        cache.pool.index_copy_(0, torch.as_tensor([int(b) for b in block_ids], dtype=torch.long), pages)
-        return
-    if not pages.is_cuda or not pages.is_contiguous() or pages.dtype != torch.uint8:
+    if not cache.pool.is_cuda or not pages.is_cuda or not pages.is_contiguous() or pages.dtype != torch.uint8:
         raise ValueError("import_pages: pages must be a contiguous uint8 CUDA tensor")
     n = len(block_ids)
     if n:
@@ -75,20 +73,20 @@ def import_pages(cache: PagedKVCache, block_ids: Sequence[int], pages: torch.Ten
 
 
 def send_sequence(cache: PagedKVCache, alloc: BlockAllocator, seq_id, dst: int,
-                  group: Optional[dist.ProcessGroup] = None) -> int:
+                  group: Optional[dist.ProcessGroup] = None, export=export_pages) -> int:
     """Send ``seq_id``'s length and pages to rank ``dst``; returns payload bytes."""
     blocks = alloc.block_ids(seq_id)
     header = torch.tensor([alloc.seq_len(seq_id), len(blocks)], dtype=torch.int64, device=cache.device)
     dist.send(header, dst, group=group)
     if blocks:
-        pages = export_pages(cache, blocks)
+        pages = export(cache, blocks)
         dist.send(pages, dst, group=group)
         return pages.numel()
     return 0
 
 
 def recv_sequence(cache: PagedKVCache, alloc: BlockAllocator, seq_id, src: int,
-                  group: Optional[dist.ProcessGroup] = None) -> List[int]:
+                  group: Optional[dist.ProcessGroup] = None, import_=import_pages) -> List[int]:
     """Receive a sequence from rank ``src`` into freshly allocated blocks of
     this worker's pool (``alloc.allocate`` + ``append_slots``); returns the
     new block ids.  Raises :class:`CacheThrashError` (nothing received into
@@ -110,5 +108,5 @@ def recv_sequence(cache: PagedKVCache, alloc: BlockAllocator, seq_id, src: int,
     if len(blocks) != nblocks:
         raise RuntimeError("sender and receiver disagree on the block count")
     if nblocks:
-        import_pages(cache, blocks, pages)
+        import_(cache, blocks, pages)
     return blocks

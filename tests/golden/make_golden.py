@@ -150,6 +150,58 @@ def ref_trace(seed: int, n_ops: int, cap_blocks: int):
     return {"seed": seed, "cap_blocks": cap_blocks, "ops": ops}
 
 
+def ref_host_trace(seed: int, n_ops: int, gpu_blocks: int, cpu_blocks: int):
+    """The reference's GPU + LOCAL_CPU tiers with writeback_on_evict: GPU
+    evictions demote to the host only when absent there and only when they fit
+    without cascading (tiered_cache.py:254-275); fetch_to_gpu promotes a host
+    hit back and keeps the host copy (tiered_cache.py:277-317).  Full blocks
+    only (the prefix-hashed pages the host tier holds)."""
+    from servesim.errors import CacheThrashError
+    from servesim.tiered_cache import CacheTier, TierConfig, TieredCacheStore
+    size = 4224
+    cfg = TierConfig(capacities={CacheTier.GPU: gpu_blocks * size, CacheTier.LOCAL_CPU: cpu_blocks * size,
+                                 CacheTier.REMOTE_CPU: None, CacheTier.DIST_STORE: None},
+                     block_size=16, writeback_on_evict=True)
+    st = TieredCacheStore(cfg)
+    rng = random.Random(seed)
+    keys = list(range(1, 3 * (gpu_blocks + cpu_blocks)))
+    ops = []
+    clock = 0
+    for _ in range(n_ops):
+        clock += rng.randrange(0, 3)
+        op = rng.choice(["insert", "insert", "fetch", "fetch", "fetch", "release", "release", "evict"])
+        k = rng.choice(keys)
+        on_cpu = sorted(h for h in st._entries if CacheTier.LOCAL_CPU in st._entries[h])
+        held = sorted(h for h, by in st._entries.items() if CacheTier.GPU in by and by[CacheTier.GPU].ref_count)
+        if op == "fetch" and on_cpu and rng.random() < 0.5:
+            k = rng.choice(on_cpu)          # exercise promotion
+        if op == "release" and held and rng.random() < 0.8:
+            k = rng.choice(held)
+        rec = {"op": op, "key": k, "clock": clock}
+        try:
+            if op == "insert":
+                st.insert(k, CacheTier.GPU, size, 16, clock)
+            elif op == "fetch":
+                plan = st.fetch_to_gpu(k, clock)
+                rec["hit"] = None if plan.hit_tier is None else plan.hit_tier.name
+            elif op == "release":
+                st.release_and_update([k], clock)
+            elif op == "evict":
+                rec["evicted"] = st.evict(CacheTier.GPU, size)
+            rec["outcome"] = "ok"
+        except CacheThrashError as e:
+            rec["outcome"] = f"thrash:{e.bytes_needed // size}"
+        except ValueError as e:
+            rec["outcome"] = f"ValueError:{e}"
+        except KeyError:
+            rec["outcome"] = "KeyError"
+        rec["gpu"] = {str(h): e.ref_count for h, e in st.resident_hashes(CacheTier.GPU).items()
+                      if e.tier == CacheTier.GPU}
+        rec["cpu"] = sorted(h for h in st._entries if CacheTier.LOCAL_CPU in st._entries[h])
+        ops.append(rec)
+    return {"seed": seed, "gpu_blocks": gpu_blocks, "cpu_blocks": cpu_blocks, "ops": ops}
+
+
 def main():
     kat()
     try:
@@ -159,6 +211,9 @@ def main():
     traces = [ref_trace(s, 400, cap) for s, cap in ((1, 6), (2, 10), (3, 4), (4, 24))]
     (HERE / "ref_block_trace.json").write_text(json.dumps(traces))
     print("ref_block_trace.json:", sum(len(t["ops"]) for t in traces), "ops")
+    host = [ref_host_trace(s, 400, g, c) for s, g, c in ((11, 4, 3), (12, 6, 1), (13, 8, 10), (14, 3, 6))]
+    (HERE / "ref_host_trace.json").write_text(json.dumps(host))
+    print("ref_host_trace.json:", sum(len(t["ops"]) for t in host), "ops")
 
 
 if __name__ == "__main__":

@@ -64,14 +64,19 @@ def check(out, ref):
     assert (err <= 2e-3 * scale + 1e-6).all(), float((err / (scale + 1e-9)).max())
 
 
-@pytest.mark.parametrize("name", ["c2", "c3_1gpu"])
+@pytest.mark.parametrize("name", ["c2", "c3_1gpu", "c4_1gpu"])
 def test_full_size_sampled_parity_and_properties(cuda, name):
+    """C4 (B = 64 x 131,072, 64 q / 4 kv heads, g = 16, INT8: 8.86 GB of pages)
+    runs the g > 8 variant at 512-page splits over 256 splits per sequence."""
     if name == "c2":
         lens = np.random.default_rng(3).integers(512, 8193, size=256) + 1
         Hq, Hkv, kvd, kvo = 32, 8, "int8", O.INT8
-    else:
+    elif name == "c3_1gpu":
         lens = np.full(128, 32769)
         Hq, Hkv, kvd, kvo = 64, 8, "fp8_e4m3", O.FP8_E4M3
+    else:
+        lens = np.full(64, 131073)
+        Hq, Hkv, kvd, kvo = 64, 4, "int8", O.INT8
     cache, table, lens, q = build(cuda, lens, Hq, Hkv, kvd, seed=11)
     tab = torch.from_numpy(table).to(cuda)
     sl = torch.from_numpy(lens.astype(np.int32)).to(cuda)
@@ -83,7 +88,8 @@ def test_full_size_sampled_parity_and_properties(cuda, name):
     alt = paged_decode_attention(q, cache, tab, sl, out_dtype=torch.float32, pages_per_split=13)
     o, a = out.cpu().numpy(), alt.cpu().numpy()
     assert (np.abs(o - a).max(-1) <= 2e-3 * np.abs(o).max(-1) + 1e-6).all(), "split invariance"
-    idx = np.random.default_rng(0).choice(len(lens), size=6 if name == "c2" else 2, replace=False)
+    idx = np.random.default_rng(0).choice(len(lens), size={"c2": 6, "c3_1gpu": 2, "c4_1gpu": 3}[name],
+                                          replace=False)
     check(o[idx], oracle_subset(cache, table, lens, q, idx, Hkv, kvo))
 
 

@@ -46,21 +46,30 @@ def _worker(rank, world, port, mode, result_q):
         dist.init_process_group("gloo", rank=rank, world_size=world)
         dev = torch.device("cuda:0")
         torch.cuda.set_device(dev)
+        kvo = O.INT8
         if mode == "head":      # KV-head tensor parallelism (Hkv % P == 0)
             Hq, Hkv, lens = 32, 8, [70, 33, 150, 0, 400, 17]
         elif mode == "batch":   # one KV head, batch halves balanced by LPT (seq_map)
             Hq, Hkv, lens = 8, 1, [70, 33, 150, 0, 400, 17, 260]
-        else:                   # 2-D at world 4: 2 KV-head groups x 2 LPT batch parts (the C4-at-8 shape)
+        elif mode == "2d":      # 2-D at world 4: 2 KV-head groups x 2 LPT batch parts (the C4-at-8 shape)
             Hq, Hkv, lens = 16, 2, [70, 33, 150, 0, 400, 17, 260, 90]
-        sc = Scenario(lens, Hq, Hkv, O.INT8, seed=9)          # identical bytes on every rank
+        elif mode == "c3p8":    # C3 at P = 8: Qwen2.5-72B heads (64 q / 8 kv), FP8, one kv head per rank
+            Hq, Hkv, kvo = 64, 8, O.FP8_E4M3
+            lens = [int(x) for x in np.random.default_rng(31).integers(1, 900, size=12)]
+        else:                   # c4p8 -- C4 at P = 8: Qwen3-235B heads (64 q / 4 kv, g = 16), INT8,
+            Hq, Hkv = 64, 4     # 4 kv-head groups x 2 LPT batch parts
+            lens = [int(x) for x in np.random.default_rng(41).integers(1, 1500, size=11)]
+        sc = Scenario(lens, Hq, Hkv, kvo, seed=9)             # identical bytes on every rank
+        kvd = "fp8_e4m3" if kvo == O.FP8_E4M3 else "int8"
         B = sc.B
         pps = 4
         plan = plan_shards(Hq, Hkv, world, rank, sc.seq_lens)
         (k0, k1), (q0, q1) = plan.kv_range, plan.q_range
+        checks["plan"] = (plan.h_split, plan.b_split)
         seqs = torch.as_tensor(plan.seqs)
-        full_cache = PagedKVCache(KVCacheSpec(Hkv), sc.num_blocks, device=dev,
+        full_cache = PagedKVCache(KVCacheSpec(Hkv, kv_dtype=kvd), sc.num_blocks, device=dev,
                                   pool=torch.from_numpy(sc.pool).to(dev))
-        loc_cache = PagedKVCache(KVCacheSpec(k1 - k0), sc.num_blocks, device=dev,
+        loc_cache = PagedKVCache(KVCacheSpec(k1 - k0, kv_dtype=kvd), sc.num_blocks, device=dev,
                                  pool=torch.from_numpy(np.ascontiguousarray(sc.pool[:, k0:k1])).to(dev))
         table_full = torch.from_numpy(sc.block_table).to(dev)
         lens_full = torch.from_numpy(sc.seq_lens).to(dev)
@@ -163,8 +172,13 @@ def test_peer_setup_failure_is_collective(cuda):
     assert res == {0: "raised", 1: "raised"}
 
 
-@pytest.mark.parametrize("mode,world", [("head", 2), ("batch", 2), ("2d", 4)])
+PLANS = {"head": (2, 1), "batch": (1, 2), "2d": (2, 2), "c3p8": (8, 1), "c4p8": (4, 2)}
+
+
+@pytest.mark.parametrize("mode,world", [("head", 2), ("batch", 2), ("2d", 4), ("c3p8", 8), ("c4p8", 8)])
 def test_fused_peer_gather_ranks_on_one_gpu(cuda, mode, world):
+    """world 8 runs the two production P = 8 plans at reduced batch: C3 (one
+    kv head per rank) and C4 (4 kv-head groups x 2 LPT batch parts, g = 16)."""
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
@@ -181,4 +195,5 @@ def test_fused_peer_gather_ranks_on_one_gpu(cuda, mode, world):
     for r in range(world):
         c = res[r]
         assert "exception" not in c, c
-        assert c == {"eager": True, "graph": True, "session": True, "no_timeouts": True}, (r, c)
+        assert c == {"plan": PLANS[mode], "eager": True, "graph": True, "session": True, "no_timeouts": True}, \
+            (r, c)

@@ -1,6 +1,7 @@
 """§8f-3: prefix reuse of quantized pages (chained block keys, natively
 computed, pinned to the reference's hash) and the pinned-host tier for evicted
 pages (payload round trips bit-identically)."""
+import json
 import random
 import sys
 from pathlib import Path
@@ -127,3 +128,114 @@ def test_random_prefix_workload_invariants(seed):
         alloc.check_invariants()
         for sid, toks in live.items():
             assert alloc.seq_len(sid) == len(toks)
+
+
+GOLDEN = Path(__file__).resolve().parent / "golden"
+
+
+def _pattern(k: int) -> torch.Tensor:
+    from paper_2605_29639_b200._lib import PAGE_BYTES
+    return ((torch.arange(PAGE_BYTES) * 7 + k * 13) % 251).to(torch.uint8).view(1, PAGE_BYTES)
+
+
+@pytest.mark.parametrize("trace", range(4))
+def test_host_tier_replays_reference_trace(trace):
+    """The reference's own GPU + LOCAL_CPU tiers with writeback_on_evict
+    (tests/golden/ref_host_trace.json, made by servesim.tiered_cache): demotion
+    only when absent and only without cascading (tiered_cache.py:254-275),
+    promotion keeps the host copy (277-317).  Replayed through PrefixKVCache's
+    own eviction hook and _promote, with every page's bytes checked after each
+    promotion (a promoted page must carry its own key's bytes)."""
+    from paper_2605_29639_b200.cache import CacheThrashError
+    tr = json.loads((GOLDEN / "ref_host_trace.json").read_text())[trace]
+    pkv = PrefixKVCache(KVCacheSpec(1), tr["gpu_blocks"], device="cpu", host_blocks=tr["cpu_blocks"])
+    pool = pkv.alloc.pool
+    for i, rec in enumerate(tr["ops"]):
+        k, clock = rec["key"], rec["clock"]
+        key = ("h", k)
+        pkv.alloc.clock = clock
+        hit = None
+        try:
+            if rec["op"] == "insert":
+                pkv.cache.pool[pool.insert(key, 16, clock)] = _pattern(k)
+            elif rec["op"] == "fetch":
+                if pool.entry(key) is not None:
+                    hit = "GPU"
+                elif key in pkv.host:
+                    hit = "LOCAL_CPU"
+                    assert pkv._promote(key)
+                    assert torch.equal(pkv.cache.pool[pool.lookup(key)], _pattern(k)), (i, "promoted bytes")
+                if hit is not None:
+                    pool.acquire(key, clock)
+            elif rec["op"] == "release":
+                pool.release([key], clock)
+            elif rec["op"] == "evict":
+                assert pool.evict(1) == [("h", e) for e in rec["evicted"]], i
+            outcome = "ok"
+        except CacheThrashError as e:
+            outcome = f"thrash:{e.bytes_needed // pool.bytes_per_block}"
+        except ValueError as e:
+            outcome = f"ValueError:{e}"
+        except KeyError:
+            outcome = "KeyError"
+        assert outcome == rec["outcome"], (i, rec, outcome)
+        if "hit" in rec:
+            assert hit == rec["hit"], (i, rec, hit)
+        assert {str(kk[1]): e.ref_count for kk, e in pool._entries.items()} == rec["gpu"], (i, rec)
+        assert sorted(kk[1] for kk in pkv.host.keys()) == rec["cpu"], (i, rec)
+
+
+def test_decoding_without_token_ids_stops_prefix_hashing():
+    """A prefix-admitted sequence decoded with append_one (ids unknown) must not
+    key the pages it fills: a later prompt sharing only the admitted tokens
+    reuses the admitted full pages and nothing past them."""
+    spec = KVCacheSpec(1)
+    pkv = PrefixKVCache(spec, 32, device="cpu")
+    a = list(range(100, 140))                       # 2 full pages + 8 tokens
+    assert pkv.admit("A", a)[0] == 0
+    for _ in range(8):                              # fills page 2 with decoded tokens
+        pkv.alloc.append_one(["A"])
+    pkv.alloc.append_slots("A", 20)                 # and pages past it
+    pkv.free("A")
+    b = a + [7] * 8                                 # same 40 tokens, different 8 after them
+    cached, _ = pkv.admit("B", b)
+    assert cached == 32
+    pkv.alloc.check_invariants()
+    with pytest.raises(ValueError, match="without token ids"):
+        pkv.alloc.allocate("C")
+        pkv.alloc.append_slots("C", 3)
+        pkv.alloc.append_tokens("C", [1, 2])
+
+
+def test_admit_releases_everything_on_thrash():
+    """CacheThrashError inside admit leaves no sequence and no extra references
+    (the reference releases what it acquired, simulator.py:397-400), so the
+    request can be retried."""
+    from paper_2605_29639_b200.cache import CacheThrashError
+    pkv = PrefixKVCache(KVCacheSpec(1), 6, device="cpu")
+    shared = list(range(500, 532))                  # 2 pages, cached after free
+    pkv.admit("P", shared)
+    pkv.alloc.allocate("hog")
+    pkv.alloc.append_slots("hog", 3 * 16)           # 3 private pages pinned
+    pkv.free("P")
+    refs = [pkv.alloc.ref_count(b) for b in range(6)]
+    with pytest.raises(CacheThrashError):
+        pkv.admit("R", shared + list(range(64)))    # shares 2 pages, then needs 4 more of 1 free
+    assert "R" not in pkv.alloc
+    assert [pkv.alloc.ref_count(b) for b in range(6)] == refs
+    pkv.alloc.check_invariants()
+    pkv.free("hog")
+    assert pkv.admit("R", shared + list(range(64)))[0] == 32   # the retry succeeds
+
+
+def test_promotion_with_a_one_block_host_tier():
+    """The promoted page keeps its own bytes when the GPU insert behind the
+    promotion evicts (and tries to demote) another page into a full host tier."""
+    pkv = PrefixKVCache(KVCacheSpec(1), 1, device="cpu", host_blocks=1)
+    pool = pkv.alloc.pool
+    pkv.cache.pool[pool.insert(("h", 1), 16, 1)] = _pattern(1)
+    pool.evict(1)                                    # ("h", 1) demoted into the single host slot
+    pkv.cache.pool[pool.insert(("h", 2), 16, 2)] = _pattern(2)
+    assert pkv._promote(("h", 1))                    # evicts ("h", 2): host full, dropped
+    assert torch.equal(pkv.cache.pool[pool.lookup(("h", 1))], _pattern(1))
+    assert pkv.host.keys() == [("h", 1)] and pkv.host.dropped == 1

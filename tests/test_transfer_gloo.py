@@ -17,6 +17,15 @@ def _free_port():
         return s.getsockname()[1]
 
 
+def host_export(cache, block_ids):
+    """Test-side page copy for CPU pools (the product path is kvq_gather_blocks)."""
+    return cache.pool.index_select(0, torch.as_tensor([int(b) for b in block_ids], dtype=torch.long))
+
+
+def host_import(cache, block_ids, pages):
+    cache.pool.index_copy_(0, torch.as_tensor([int(b) for b in block_ids], dtype=torch.long), pages)
+
+
 def _worker(rank, port, q):
     import sys
     from pathlib import Path
@@ -39,13 +48,13 @@ def _worker(rank, port, q):
         slots = np.asarray(alloc.append_slots("req", L), dtype=np.int32)
         pool = cache.pool.numpy()
         O.quant_append(bf16_bits(k), bf16_bits(v), slots, O.FP8_E4M3, pool)
-        sent = send_sequence(cache, alloc, "req", 1)
+        sent = send_sequence(cache, alloc, "req", 1, export=host_export)
         q.put((rank, sent, sent == -(-L // 16) * Hkv * 4224, wire_bytes_per_token(Hkv) * 2 == Hkv * 264 * 2))
     else:                                           # decode worker
         alloc = BlockAllocator(20)
         cache = PagedKVCache(spec, 20, device="cpu")
         alloc.allocate("other"); alloc.append_slots("other", 5)
-        blocks = recv_sequence(cache, alloc, "req", 0)
+        blocks = recv_sequence(cache, alloc, "req", 0, import_=host_import)
         # expected: the same rows quantized on the CPU into this worker's block ids
         exp = np.zeros((20, Hkv, 4224), np.uint8)
         tok = np.arange(L)

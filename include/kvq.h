@@ -40,7 +40,8 @@
 extern "C" {
 #endif
 
-#define KVQ_ABI_VERSION 2 /* 2: peer gather, decode_step (+flags), pipeline submitter, block gather/scatter */
+#define KVQ_ABI_VERSION 3 /* 2: peer gather, decode_step (+flags), pipeline submitter, block gather/scatter;
+                             3: kvq_check_device_errors, kvq_profile_next_decode */
 #define KVQ_HEAD_DIM 128  /* d */
 #define KVQ_BLOCK_SIZE 16 /* tokens per page */
 #define KVQ_PAGE_BYTES 4224 /* one (block, kv head): 2x16x128 codes + 2x16 fp32 scales */
@@ -53,6 +54,32 @@ enum kvq_out_layout { KVQ_OUT_BHD = 0 /* [B][Hq][d] */, KVQ_OUT_HBD = 1 /* [Hq][
 int kvq_version(void);
 const char* kvq_last_error(void);
 size_t kvq_page_bytes(void);
+
+/* Caller errors the kernels can only see on the device.  The kernels never
+ * fault on them: an out-of-range block id is read as block 0, a length past
+ * max_blocks * 16 is clamped, a slot past the pool is skipped -- and a bit is
+ * set in a device-side error word:
+ *   KVQ_DERR_BLOCK_ID  K2 met block_table[b][i] outside [0, num_blocks) among
+ *                      a sequence's visible pages;
+ *   KVQ_DERR_SEQ_LEN   K2 met seq_lens[b] > max_blocks * 16 or < 0;
+ *   KVQ_DERR_SLOT      K1 (or the fused append) met slot >= 0 with
+ *                      slot / 16 >= num_blocks (slot < 0 is "skip", not an error).
+ * kvq_check_device_errors synchronizes `stream`, reads and clears the word
+ * (all kernels of this process on the current device), and returns KVQ_OK, or
+ * KVQ_EINVAL with the bits in kvq_last_error() and in *bits (may be NULL).
+ * It synchronizes: a validation / debug call, not for the step path.  The
+ * oracle abort()s on the same inputs (oracle/kvq_oracle.c). */
+enum kvq_device_error { KVQ_DERR_BLOCK_ID = 1, KVQ_DERR_SEQ_LEN = 2, KVQ_DERR_SLOT = 4 };
+int kvq_check_device_errors(void* stream, uint32_t* bits);
+
+/* Profiling (bench.py's roofline): the next K2 launch this host thread issues
+ * (kvq_decode_attn*, kvq_decode_step*) records its grid span in device memory:
+ * span[0] = min over CTAs of the start %globaltimer, span[1] = max end (ns).
+ * The caller sets span[0] = UINT64_MAX, span[1] = 0 beforehand.  One-shot; the
+ * pointer is a kernel parameter, so a CUDA-graph capture keeps it (one span
+ * per captured launch) and the kernel times itself inside a PDL-chained step.
+ * NULL cancels a pending request. */
+int kvq_profile_next_decode(uint64_t* span);
 
 /* Quantize-on-append (K1).  k, v: bf16 [T][Hkv][128] with token strides
  * k_token_stride / v_token_stride (in elements; head stride is 128, rows

@@ -8,11 +8,11 @@ ABI of ``libkvq.so`` (include/kvq.h).
 """
 from .cache import (BlockAllocator, BlockTable, CacheThrashError, KVCacheSpec, PagedKVCache,
                     unpack_pages)
-from .ops import copy_blocks, decode_step, paged_decode_attention, paged_decode_attention_gathered, quantize_append
+from .ops import check_device_errors, copy_blocks, decode_step, paged_decode_attention, paged_decode_attention_gathered, quantize_append
 
 __all__ = [
     "BlockAllocator", "BlockTable", "CacheThrashError", "KVCacheSpec", "PagedKVCache",
-    "unpack_pages", "copy_blocks", "decode_step", "paged_decode_attention", "paged_decode_attention_gathered",
+    "unpack_pages", "check_device_errors", "copy_blocks", "decode_step", "paged_decode_attention", "paged_decode_attention_gathered",
     "quantize_append",
 ]
 __version__ = "0.1.0"

@@ -622,24 +622,54 @@ class BlockTable:
     updated incrementally: each row remembers which sequence it holds and how
     many of its block ids are already on the device, so a decode step moves
     only the block ids appended since the last sync (a few per step) and the
-    lengths, instead of rebuilding the table."""
+    lengths, instead of rebuilding the table.
 
-    def __init__(self, max_seqs: int, max_blocks: int, device="cuda"):
+    The host never waits for the device: the delta (flat index, block id) and
+    the lengths are written into a pinned staging slot (a ring of ``depth``),
+    copied host-to-device with ``non_blocking`` copies -- on ``copy_stream``
+    when given, so the transfer overlaps the kernels still running -- and
+    scattered into the table on the current (compute) stream, which orders
+    the update after every earlier kernel that reads the table and before
+    every later one."""
+
+    def __init__(self, max_seqs: int, max_blocks: int, device="cuda", depth: int = 2):
         self.max_seqs, self.max_blocks = max_seqs, max_blocks
+        self.device = torch.device(device)
         self.table = torch.zeros((max_seqs, max_blocks), dtype=torch.int32, device=device)
         self.seq_lens = torch.zeros((max_seqs,), dtype=torch.int32, device=device)
         self._row_seq: List[object] = [None] * max_seqs   # the _Seq a row holds
         self._row_n = np.zeros((max_seqs,), dtype=np.int64)  # its block ids already on the device
         self._host_lens = np.zeros((max_seqs,), dtype=np.int32)
+        self._depth = max(1, depth)
+        self._ring: List[dict] = []
+        self._next = 0
+        self._grow(max(64, max_seqs))
 
-    def sync(self, alloc: BlockAllocator, seq_ids: Sequence) -> int:
+    def _grow(self, cap: int) -> None:
+        """(Re)allocate the staging ring for ``cap`` updates per sync."""
+        cuda = self.device.type == "cuda"
+        for r in self._ring:   # the old slots may still feed in-flight copies
+            if r["copied"] is not None:
+                r["copied"].synchronize()
+        self._cap = cap
+        self._ring = []
+        for _ in range(self._depth):
+            host = torch.empty((2 * cap + self.max_seqs,), dtype=torch.int64, pin_memory=cuda)
+            dev = torch.empty_like(host, device=self.device)
+            self._ring.append(dict(host=host, hnp=host.numpy(), dev=dev, copied=None, used=None))
+
+    def sync(self, alloc: BlockAllocator, seq_ids: Sequence, copy_stream=None) -> int:
         """Push the rows of ``seq_ids`` (row i <- seq_ids[i]); returns the
-        number of table entries transferred."""
+        number of table entries transferred.  Asynchronous (see the class
+        docstring); with ``copy_stream`` the current stream waits for the copy
+        before the scatter."""
         n = len(seq_ids)
         if n > self.max_seqs:
             raise ValueError("more sequences than table rows")
-        rows, cols, vals = [], [], []
+        idx: List[int] = []
+        vals: List[int] = []
         lens = np.empty((n,), dtype=np.int32)
+        mb = self.max_blocks
         for i, sid in enumerate(seq_ids):
             s = alloc._seq(sid)
             if self._row_seq[i] is not s:       # row now holds another sequence: rewrite it
@@ -648,18 +678,49 @@ class BlockTable:
             b = s.blocks
             k0 = int(self._row_n[i])
             if len(b) > k0:
-                if len(b) > self.max_blocks:
+                if len(b) > mb:
                     raise ValueError("max_blocks too small")
-                rows.extend([i] * (len(b) - k0))
-                cols.extend(range(k0, len(b)))
+                idx.extend(range(i * mb + k0, i * mb + len(b)))
                 vals.extend(b[k0:])
                 self._row_n[i] = len(b)
             lens[i] = s.length
-        if rows:
-            upd = torch.from_numpy(np.array([rows, cols, vals], dtype=np.int64))
-            upd = upd.to(self.table.device, non_blocking=False)
-            self.table[upd[0], upd[1]] = upd[2].to(torch.int32)
-        if not np.array_equal(lens, self._host_lens[:n]):
-            self.seq_lens[:n].copy_(torch.from_numpy(lens))
+        new_lens = not np.array_equal(lens, self._host_lens[:n])
+        if not idx and not new_lens:
+            return 0
+        if len(idx) > self._cap:
+            self._grow(max(len(idx), 2 * self._cap))
+        r = self._ring[self._next]
+        self._next = (self._next + 1) % self._depth
+        if r["copied"] is not None:
+            r["copied"].synchronize()           # its previous upload (depth syncs ago) has been read
+        m, cap = len(idx), self._cap
+        h = r["hnp"]
+        h[:m] = idx
+        h[cap:cap + m] = vals
+        h[2 * cap:2 * cap + n] = lens
+        cuda = self.device.type == "cuda"
+        cur = torch.cuda.current_stream(self.device) if cuda else None
+        cs = copy_stream if (cuda and copy_stream is not None) else cur
+        if cuda:
+            with torch.cuda.stream(cs):
+                if r["used"] is not None:
+                    cs.wait_event(r["used"])    # the scatter that read this device slot has run
+                r["dev"][:m].copy_(r["host"][:m], non_blocking=True)
+                r["dev"][cap:cap + m].copy_(r["host"][cap:cap + m], non_blocking=True)
+                r["dev"][2 * cap:2 * cap + n].copy_(r["host"][2 * cap:2 * cap + n], non_blocking=True)
+                r["copied"] = torch.cuda.Event()
+                r["copied"].record(cs)
+            if cs is not cur:
+                cur.wait_event(r["copied"])
+        else:
+            r["dev"][:2 * cap + n].copy_(r["host"][:2 * cap + n])
+        d = r["dev"]
+        if m:
+            self.table.view(-1).index_copy_(0, d[:m], d[cap:cap + m].to(torch.int32))
+        if new_lens:
+            self.seq_lens[:n].copy_(d[2 * cap:2 * cap + n])
             self._host_lens[:n] = lens
-        return len(rows)
+        if cuda:
+            r["used"] = torch.cuda.Event()
+            r["used"].record(cur)
+        return m

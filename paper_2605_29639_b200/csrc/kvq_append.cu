@@ -230,7 +230,10 @@ __global__ void __launch_bounds__(K1_THREADS, 3) quant_append_kernel(  // 80 reg
   // ---- scattered tokens: direct global stores
   bool live[2];
 #pragma unroll
-  for (int i = 0; i < 2; ++i) live[i] = slot[i] >= 0 && (slot[i] >> 4) < num_blocks && h < Hkv;
+  for (int i = 0; i < 2; ++i) {
+    live[i] = slot[i] >= 0 && (slot[i] >> 4) < num_blocks && h < Hkv;
+    if (slot[i] >= 0 && (slot[i] >> 4) >= num_blocks && j == 0 && hh == 0) flag_dev_err(KVQ_DERR_SLOT);
+  }
   const bool pair_adj = live[0] && live[1] && (slot[0] & 1) == 0 && slot[1] == slot[0] + 1;
 #pragma unroll
   for (int i = 0; i < 2; ++i) {
@@ -298,7 +301,10 @@ __global__ void __launch_bounds__(K1R_WARPS * 32) quant_append_rows_kernel(
     ak = fmaxf(ak, __shfl_xor_sync(FULL, ak, o));
     av = fmaxf(av, __shfl_xor_sync(FULL, av, o));
   }
-  if (slot < 0 || (slot >> 4) >= num_blocks) return;
+  if (slot < 0 || (slot >> 4) >= num_blocks) {
+    if (slot >= 0 && lane == 0) flag_dev_err(KVQ_DERR_SLOT);
+    return;
+  }
   const float qmax = KVD == KVQ_FP8_E4M3 ? 448.0f : 127.0f;
   const float ik = ak > 0.0f ? __fdiv_rn(qmax, ak) : 0.0f;
   const float iv = av > 0.0f ? __fdiv_rn(qmax, av) : 0.0f;
@@ -313,6 +319,8 @@ __global__ void __launch_bounds__(K1R_WARPS * 32) quant_append_rows_kernel(
     *reinterpret_cast<float*>(page + (lane ? VS_OFF : KS_OFF) + 4 * tok) = __fdiv_rn(a, qmax);
   }
 }
+
+unsigned read_and_clear_dev_err_append() { return read_and_clear_dev_err_tu(); }
 
 }  // namespace kvq
 

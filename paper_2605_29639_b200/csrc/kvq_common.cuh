@@ -197,6 +197,23 @@ __device__ __forceinline__ void codes_to_f16x2(uint32_t w, uint32_t& lo, uint32_
   }
 }
 
+// Device-side caller-error word (kvq_check_device_errors): kernels that meet
+// an argument they cannot honour (an out-of-range block id, slot or length)
+// still do something safe (skip / clamp) but OR a bit in here.  One copy per
+// translation unit (no relocatable device code); each TU that sets bits
+// exports a reader, read_and_clear_dev_err().
+static __device__ unsigned int g_dev_err;
+__device__ __forceinline__ void flag_dev_err(unsigned bit) { atomicOr(&g_dev_err, bit); }
+static inline unsigned read_and_clear_dev_err_tu() {
+  unsigned v = 0;
+  const unsigned zero = 0;
+  if (cudaMemcpyFromSymbol(&v, g_dev_err, sizeof(v)) != cudaSuccess) return 0x80000000u;
+  if (v && cudaMemcpyToSymbol(g_dev_err, &zero, sizeof(zero)) != cudaSuccess) return v | 0x80000000u;
+  return v;
+}
+unsigned read_and_clear_dev_err_append();
+unsigned read_and_clear_dev_err_decode();
+
 }  // namespace kvq
 
 // C-ABI error reporting: a thread-local message behind kvq_last_error().

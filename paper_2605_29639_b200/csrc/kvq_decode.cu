@@ -43,6 +43,9 @@ struct DecodeParams {
   const __nv_bfloat16* av;
   int64_t ak_stride, av_stride;
   const int32_t* aslots;
+  // kvq_profile_next_decode: when set, the grid's span (min CTA start, max CTA
+  // end, %globaltimer ns) is recorded here; nullptr for every ordinary launch.
+  unsigned long long* span;
 };
 
 constexpr int NW = 4;  // warps per CTA; every warp streams its own pages
@@ -215,7 +218,10 @@ struct PageStream {
   __device__ __forceinline__ int load_ids(int j0, int lane) const {
     const int j = j0 + lane;
     int blk = j < nj ? __ldg(bt + warp + j * NW) : 0;
-    if ((unsigned)blk >= (unsigned long long)num_blocks) blk = 0;
+    if ((unsigned)blk >= (unsigned long long)num_blocks) {  // caller error: read block 0, report
+      flag_dev_err(KVQ_DERR_BLOCK_ID);
+      blk = 0;
+    }
     return blk;
   }
   __device__ __forceinline__ void init(int lane) {
@@ -263,7 +269,9 @@ __device__ __forceinline__ void decode_cta(const DecodeParams& p, uint8_t* smem)
   const int split = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
   // MQ: q_len > 1 query tokens per sequence (compile-time off for plain decode).
   const int g = p.g, G = MQ ? p.G : p.g, qlen = MQ ? p.q_len : 1;
-  const int L = min(__ldg(p.seq_lens + b), p.max_blocks * BS);
+  const int L_in = __ldg(p.seq_lens + b);
+  const int L = min(L_in, p.max_blocks * BS);
+  if ((L_in > L || L_in < 0) && threadIdx.x == 0 && blockIdx.x == 0) flag_dev_err(KVQ_DERR_SEQ_LEN);
   const int npages = (L + BS - 1) / BS;
   const int nsplit = max(1, (npages + p.pages_per_split - 1) / p.pages_per_split);
   if (split >= nsplit) return;
@@ -365,7 +373,12 @@ __device__ __forceinline__ void decode_cta(const DecodeParams& p, uint8_t* smem)
       patch[2 * lane] = ck;
       patch[2 * lane + 1] = cv;
       if (lane < 2) patch[64 + lane] = __float_as_uint(sc);
-      if (aslot >= 0 && (aslot >> 4) < p.num_blocks) {
+      // An invalid slot is skipped, as K1 does: the row reaches neither the pool
+      // nor this CTA's copy of the page (so the output equals K1 + K2's).
+      if (aslot < 0 || (aslot >> 4) >= p.num_blocks) {
+        patch_j = -1;
+        if (aslot >= 0 && lane == 0 && h == 0) flag_dev_err(KVQ_DERR_SLOT);
+      } else {
         uint8_t* page = const_cast<uint8_t*>(p.pool) + ((int64_t)(aslot >> 4) * p.Hkv + h) * PAGE;
         const int tok = aslot & 15;
         *reinterpret_cast<uint32_t*>(page + k_code_off(tok, 4 * lane)) = ck;
@@ -981,9 +994,14 @@ __global__ void __launch_bounds__(THREADS, Geo<HI>::CTAS) decode_kernel(const De
   unsigned long long t0 = 0;
   if (threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
 #endif
+  if (p.span && threadIdx.x == 0) atomicMin(p.span, global_ns());
   if (MODE == 2 && threadIdx.x == 0) peer_release(p.peer);
   decode_cta<KVD, HI, MODE>(p, smem);
   if (MODE == 2 && threadIdx.x == 0) peer_arrive(p.peer);
+  if (p.span) {  // CTA-uniform: every path out of decode_cta is
+    __syncthreads();
+    if (threadIdx.x == 0) atomicMax(p.span + 1, global_ns());
+  }
 #ifdef KVQ_TIMELINE
   if (threadIdx.x == 0) {
     unsigned long long t1;
@@ -999,6 +1017,8 @@ __global__ void __launch_bounds__(THREADS, Geo<HI>::CTAS) decode_kernel(const De
   }
 #endif
 }
+
+unsigned read_and_clear_dev_err_decode() { return read_and_clear_dev_err_tu(); }
 
 }  // namespace kvq
 
@@ -1107,6 +1127,9 @@ static cudaError_t set_attributes_once(const void* kernel, int smem_bytes) {
   return e;
 }
 
+// kvq_profile_next_decode: one-shot span pointer for this host thread's next K2 launch.
+static thread_local unsigned long long* t_next_span = nullptr;
+
 static int decode_attn_impl(const void* q, int64_t q_batch_stride, int32_t q_len, const void* pool,
                             int64_t num_blocks, const int32_t* block_table, int32_t max_blocks,
                             const int32_t* seq_lens, int32_t B, int32_t Hq, int32_t Hkv, int32_t kv_dtype,
@@ -1174,6 +1197,8 @@ static int decode_attn_impl(const void* q, int64_t q_batch_stride, int32_t q_len
   prm.ak_stride = fk_stride;
   prm.av_stride = fv_stride;
   prm.aslots = fslots;
+  prm.span = t_next_span;
+  t_next_span = nullptr;
 
   const dim3 grid((unsigned)max_splits, (unsigned)Hkv, (unsigned)B);
   auto st = static_cast<cudaStream_t>(stream);
@@ -1316,6 +1341,12 @@ int kvq_decode_attn(const void* q, int64_t q_batch_stride, const void* pool, int
   return kvq_decode_attn_mq(q, q_batch_stride, 1, pool, num_blocks, block_table, max_blocks, seq_lens,
                             B, Hq, Hkv, kv_dtype, sm_scale, pages_per_split, workspace, workspace_bytes,
                             out, out_dtype, out_layout, stream);
+}
+
+int kvq_profile_next_decode(uint64_t* span) {
+  if (span && !aligned(span, 8)) return fail(KVQ_EINVAL, "profile_next_decode: span must be 8-byte aligned");
+  t_next_span = reinterpret_cast<unsigned long long*>(span);
+  return KVQ_OK;
 }
 
 #ifdef KVQ_TIMELINE

@@ -61,6 +61,21 @@ const char* kvq_last_error(void) { return g_err; }
 
 size_t kvq_page_bytes(void) { return KVQ_PAGE_BYTES; }
 
+int kvq_check_device_errors(void* stream, uint32_t* bits) {
+  if (bits) *bits = 0;
+  const cudaError_t e = cudaStreamSynchronize(static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return fail(KVQ_ECUDA, cudaGetErrorString(e));
+  const unsigned v = kvq::read_and_clear_dev_err_append() | kvq::read_and_clear_dev_err_decode();
+  if (v & 0x80000000u) return fail(KVQ_ECUDA, "check_device_errors: cannot read the device error word");
+  if (bits) *bits = v;
+  if (!v) return KVQ_OK;
+  snprintf(g_err, sizeof(g_err), "device-side caller error(s):%s%s%s",
+           (v & KVQ_DERR_BLOCK_ID) ? " block id out of range [0, num_blocks) (KVQ_DERR_BLOCK_ID);" : "",
+           (v & KVQ_DERR_SEQ_LEN) ? " seq_lens outside [0, max_blocks * 16] (KVQ_DERR_SEQ_LEN);" : "",
+           (v & KVQ_DERR_SLOT) ? " slot past the pool (KVQ_DERR_SLOT);" : "");
+  return KVQ_EINVAL;
+}
+
 int kvq_pipeline_submit(const kvq_pipe_step* s) {
   if (!s || !s->graph_exec || !s->dev_in || !s->host_in || !s->dev_out || !s->host_out || !s->ev_in_ready ||
       !s->ev_done || !s->ev_out_done)

@@ -31,6 +31,29 @@ def _stream_handle(device: torch.device) -> int:
     return raw(idx) if raw is not None else torch.cuda.current_stream(device).cuda_stream
 
 
+def check_device_errors(device=None) -> None:
+    """Raise ``ValueError`` if a kernel met an out-of-range block id, sequence
+    length or slot since the last check (``kvq_check_device_errors``: the
+    kernels skip or clamp such input instead of faulting, and report it here).
+    Synchronizes the current stream: a validation call, not for the step path."""
+    import ctypes
+    dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+    bits = ctypes.c_uint32(0)
+    _lib.check("kvq_check_device_errors", _lib.load().kvq_check_device_errors(_stream_handle(dev), ctypes.byref(bits)))
+
+
+def profile_next_decode(span: Optional[torch.Tensor]) -> None:
+    """Make this thread's next K2 launch record its grid span (start / end
+    %globaltimer, ns) into ``span`` (a CUDA uint64/int64 tensor of 2, preset
+    to (max, 0)); ``None`` cancels (``kvq_profile_next_decode``).  Capturable."""
+    if span is not None:
+        _require_cuda("profile_next_decode", span)
+        if span.dtype not in (torch.int64, torch.uint64) or span.numel() < 2:
+            raise ValueError("profile_next_decode: span must hold 2 x 64-bit")
+    _lib.check("kvq_profile_next_decode",
+               _lib.load().kvq_profile_next_decode(span.data_ptr() if span is not None else None))
+
+
 def _require_cuda(name: str, *ts: torch.Tensor) -> None:
     for t in ts:
         if not t.is_cuda:

@@ -61,3 +61,41 @@ def test_plugs_into_servesim_simulation():
     # the calibrated B200 step (~1.5 ms for 32 layers at 4K ctx) is far below the 10 ms constant
     assert meas.to_dict()["decode_span_mean_us"] < base.to_dict()["decode_span_mean_us"]
     assert meas.to_dict()["tokens_per_sec"] > base.to_dict()["tokens_per_sec"]
+
+
+def test_scoring_passes_and_factors():
+    from paper_2605_29639_b200.costmodel import append_bytes_per_token, mq_factor, scoring_passes
+    assert scoring_passes(4, 1) == [4] and scoring_passes(4, 4) == [16]
+    assert scoring_passes(4, 9) == [16, 16, 4]          # k = 8 draft tokens at g = 4: three passes
+    assert scoring_passes(16, 2) == [16, 16]
+    assert (mq_factor(4), mq_factor(8), mq_factor(16)) == (1.0, 1.02, 1.24)
+    assert append_bytes_per_token(8) == 8 * 776 + 4
+
+
+@pytest.mark.skipif(not _servesim(), reason="reference simulator not available")
+def test_spec_scoring_and_prefill_append_in_servesim():
+    """With speculative decoding on, the simulator charges spec_iteration_us
+    (simulator.py:499-502): priced here as multi-query K2 passes instead of
+    the constant spec_score_us; prefill_us gains the K1 append of every
+    computed token in every layer."""
+    from servesim.config import SimConfig, SpecSettings
+    from servesim.cost import CostModel
+    from servesim.simulator import run
+    from servesim.workload import synth_trace
+
+    f = DecodeFit(launch_us=6.0, bytes_per_us=6.5e6, points=4)
+    kw = dict(layers=32, mean_ctx_tokens=4352, kv_bytes_per_token=2112, heads_per_kv=4, num_kv_heads=8)
+    cm = make_servesim_cost_model(f, spec_q_len=4, append_bytes_per_us=2.8e6, append_launch_us=3.0, **kw)
+    plain = make_servesim_cost_model(f, **kw)
+    dec = cm.decode_step_us(8)
+    assert cm.spec_iteration_us(8) == round(cm.spec_draft_us + 32 * (6.0 + 8 * 4352 * 2112 / 6.5e6 * 1.24))
+    assert dec < cm.spec_iteration_us(8) < CostModel().spec_iteration_us(8)
+    assert plain.spec_iteration_us(8) == CostModel().spec_iteration_us(8)   # spec_q_len 0: the reference's
+    assert cm.prefill_us(2048) == CostModel().prefill_us(2048) + round(32 * (3.0 + 2048 * 6212 / 2.8e6))
+    assert plain.prefill_us(2048) == CostModel().prefill_us(2048)
+    trace = synth_trace("qa", 20, seed=1)
+    spec = SpecSettings(enabled=True, k=3)
+    base = run(trace, SimConfig(speculative=spec), seed=1).to_dict()
+    meas = run(trace, SimConfig(cost=cm, speculative=spec), seed=1).to_dict()
+    assert meas["decode_span_mean_us"] < base["decode_span_mean_us"]
+    assert meas["tokens_per_sec"] > base["tokens_per_sec"]

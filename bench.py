@@ -72,6 +72,30 @@ def algorithmic_bytes(lens, Hq_loc, Hkv_loc, B):
     return attn, append
 
 
+def cpu_model() -> str:
+    try:
+        for line in Path("/proc/cpuinfo").read_text().splitlines():
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def ncu_traffic(config: str):
+    """dram__bytes_read + write per K2 launch from profiles/ncu_traffic.json,
+    only if that capture measured THIS build (same source hash); else None."""
+    from paper_2605_29639_b200._build import source_hash
+    tp = REPO / "profiles" / "ncu_traffic.json"
+    try:
+        rec = json.loads(tp.read_text()).get(config, {})
+    except (OSError, ValueError):
+        return None, None
+    if rec.get("src_hash") != source_hash():
+        return None, rec.get("src_hash")
+    return rec.get("dram_bytes_per_launch"), rec.get("src_hash")
+
+
 def measured_peak():
     p = REPO / "MEASURED_PEAKS.json"
     if p.exists():
@@ -217,7 +241,7 @@ def run_reference(args, cfg):
         "vs_baseline": None, "dtype": cfg["kv"].replace("fp8_e4m3", "e4m3"), "data": "synthetic",
         "config": {"workload": cfg["workload"], "sample": sample.describe()},
         "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": sample.threads, "kind": "port",
-                         "sample": sample.describe()},
+                         "cpu_model": cpu_model(), "sample": sample.describe()},
         "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "note": "reference arm: the reference (servesim) has no implementation of this path "
                 "(SPEC.md:8); its CPU implementation here is the oracle port of the contract",
@@ -350,9 +374,18 @@ def run_ours(args, cfg):
     torch.cuda.synchronize()
     gather_in_graph = use_nccl and not one_gpu
 
-    # Event-record nodes cost a few microseconds of launch bubble each, so
-    # only every k2_every-th step brackets its K2 (the per-launch sample).
-    k2_every = max(1, args.k2_sample_every)
+    # K2's own duration inside the timed PDL steps: every timed K2 records its
+    # grid span (first CTA start .. last CTA end, %globaltimer) into its own
+    # slot (kvq_profile_next_decode; the pointer is a captured kernel
+    # parameter), so the roofline's kernel time comes from the very launches
+    # the step time is measured on.
+    from paper_2605_29639_b200.ops import profile_next_decode
+    spans = torch.zeros((max(args.steps, 1), 2), dtype=torch.int64, device=dev)
+
+    def reset_spans():
+        spans[:, 0] = torch.iinfo(torch.int64).max
+        spans[:, 1] = 0
+
     # A pool that fits in L2 (C1) would be timed L2-resident: instead every step
     # is preceded by a 256 MB memset that evicts L2 and bracketed by its own
     # events (the flush is outside the brackets); ms_step is their mean.
@@ -360,35 +393,25 @@ def run_ours(args, cfg):
     step_evs = []
 
     def capture_steps(n, timed):
-        evs = {}
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g):
             for i in range(n):
                 if flush_buf is not None:
                     flush_buf.zero_()
-                if flush_buf is not None and timed and i % k2_every != 0:
+                ev = None
+                if flush_buf is not None and timed:
                     ev = (torch.cuda.Event(enable_timing=True, external=True),
                           torch.cuda.Event(enable_timing=True, external=True))
                     ev[0].record()
-                    sess.step(buf)
+                if timed:
+                    profile_next_decode(spans[i])
+                sess.step(buf)  # kvq_decode_step: K2 PDL-launched behind K1 (or the fused K2 alone)
+                if ev is not None:
                     ev[1].record()
                     step_evs.append(ev)
-                elif timed and i % k2_every == 0:  # sampled step: K1, event, K2, event
-                    if not fused:
-                        sess.k1(buf)
-                    evs[i] = (torch.cuda.Event(enable_timing=True, external=True),
-                              torch.cuda.Event(enable_timing=True, external=True))
-                    evs[i][0].record()
-                    if fused:
-                        sess.step(buf)  # the fused step is one K2 launch
-                    else:
-                        sess.k2(buf)
-                    evs[i][1].record()
-                else:                            # kvq_decode_step: K2 PDL-launched behind K1
-                    sess.step(buf)
                 if gather_in_graph:
                     gather_dev(buf["out"])
-        return g, list(evs.values())
+        return g, []
 
     graphs = None
     if not use_nccl or gather_in_graph:
@@ -429,6 +452,7 @@ def run_ours(args, cfg):
                 one(evs[i])
 
     run_warm()
+    reset_spans()
     barrier()
     t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     sampler = ClockSampler(local)
@@ -442,7 +466,16 @@ def run_ours(args, cfg):
     ms_step = ms_total / args.steps
     if step_evs:  # L2-flushed steps: the mean bracketed step, not the graph span (which holds the flushes)
         ms_step = max_over_ranks(statistics.mean(a.elapsed_time(b) for a, b in step_evs))
-    k2_ms = statistics.mean(a.elapsed_time(b) for a, b in evs)
+    if evs:  # eager fallback: K2 bracketed by events
+        k2_ms = statistics.mean(a.elapsed_time(b) for a, b in evs)
+        k2_src = "CUDA events around K2 (eager fallback path, no PDL)"
+    else:
+        sp = spans.cpu().numpy()
+        ok = sp[:, 0] < np.iinfo(np.int64).max
+        k2_ms = float((sp[ok, 1] - sp[ok, 0]).mean()) / 1e6 if ok.any() else float("nan")
+        k2_src = ("grid span of every timed K2 inside the PDL step graph (first CTA start to last CTA "
+                  "end, %globaltimer; kvq_profile_next_decode)")
+    n_k2 = len(evs) if evs else int(args.steps)
     k2_ms = max_over_ranks(k2_ms)
 
     # ---- end-to-end through the public API with pinned host buffers ----------
@@ -504,6 +537,7 @@ def run_ours(args, cfg):
                 break
         dt = (time.perf_counter() - t0) / reps
         cpu = {"value": sample.B / dt, "unit": "tokens/s", "cores": sample.threads, "kind": "port",
+               "cpu_model": cpu_model(),
                "sample": sample.describe() + f"; {reps} reps, {dt * 1e3:.1f} ms/step"}
 
     peer_errors = peer.errors() if peer is not None else 0
@@ -518,13 +552,8 @@ def run_ours(args, cfg):
     attn_bytes, append_bytes = algorithmic_bytes(lens, Hq_loc, Hkv_loc, B_loc)
     peak, peak_kind = measured_peak()
     achieved = attn_bytes / (k2_ms * 1e-3) / 1e9
-    traffic = None
-    tp = REPO / "profiles" / "ncu_traffic.json"
-    if tp.exists() and world == 1:  # the committed capture is a 1-GPU launch
-        try:
-            traffic = json.loads(tp.read_text()).get(args.config, {}).get("dram_bytes_per_launch")
-        except Exception:
-            traffic = None
+    from paper_2605_29639_b200._build import source_hash
+    traffic, traffic_hash = (ncu_traffic(args.config) if world == 1 else (None, None))
     value = B / (ms_step * 1e-3)
     line = {
         "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
@@ -547,8 +576,8 @@ def run_ours(args, cfg):
                    "step": "K1 append of B rows + K2 paged decode attention (+ the gather if N>1); "
                            "stationary ctx; the K timed steps are one CUDA graph (kvq_decode_step per step: K2 "
                            "launched behind K1 with programmatic dependent launch, waiting for K1 only before "
-                           "each sequence's last page; unrolled); K2 launch time "
-                           "from event nodes around every k2_sample_every-th K2 (those steps launch K1, K2 plainly)",
+                           "each sequence's last page; unrolled); K2 time = each timed K2's own grid span "
+                           "inside that graph",
                    "e2e": "DecodeSession(graphs=True).submit_staged: one H2D of the pinned q/k/v/slots/lens "
                           "staging blob, graph of K1, K2 (, all-gather), D2H of O; double-buffered copy "
                           "streams overlap adjacent steps",
@@ -557,19 +586,182 @@ def run_ours(args, cfg):
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "kernel": "kvq::decode_kernel",
                      "algorithmic_bytes_per_launch": attn_bytes, "avg_launch_ms": k2_ms,
-                     "launches_sampled": len(evs),
+                     "launches_sampled": n_k2, "kernel_time": k2_src,
+                     "traffic_source": ("ncu --set full of this build (profiles/ncu_traffic.json, src_hash "
+                                        f"{traffic_hash})") if traffic is not None else
+                     f"none for this build (profiles/ncu_traffic.json has src_hash {traffic_hash})",
                      "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)" if peak_kind == "measured"
                      else "fallback 6.65 TB/s (B200_PROFILING.md)"},
         "e2e": {"value": B / (e2e_ms * 1e-3), "unit": "tokens/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms},
         "gpu_launches": (1 if fused else 2) * args.steps,
         "clocks": sampler.summary(),
+        "build": {"src_hash": source_hash()},
     }
     if cpu is not None:
         line["cpu_baseline"] = cpu
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+# ---------------------------------------------------------------------------
+# Serving loop: a whole model step (all layers) driven by the allocator
+# ---------------------------------------------------------------------------
+def run_serving(args, cfg):
+    """--serving: the decode loop of a model with --layers attention layers,
+    as a server runs it (simulator.py:504-517).  Per model step the host calls
+    BlockAllocator.append_one (each sequence's new slot; sequences grow),
+    BlockTable.sync (new block ids + lengths, pinned staging, copy stream) and
+    uploads the slots, then launches kvq_decode_step (K1 + PDL K2) for every
+    layer's pool.  The host never waits for the device (--table-sync legacy
+    instead synchronizes the compute stream before each sync, the round-1
+    behaviour of the pageable copies).  Reports the model step's device time
+    against the same layers replayed from a CUDA graph with no host work, and
+    the host time per step."""
+    import torch
+    from paper_2605_29639_b200 import BlockAllocator, BlockTable, KVCacheSpec, PagedKVCache, quantize_append
+    from paper_2605_29639_b200 import ops
+
+    dev = torch.device("cuda", 0)
+    torch.cuda.set_device(dev)
+    B, Hq, Hkv, layers = cfg["B"], cfg["Hq"], cfg["Hkv"], args.layers
+    lens = ctx_lens(cfg)
+    steps_total = args.warmup + args.steps + 2
+    nb = int(np.ceil((lens + steps_total) / 16).sum()) + B + 16
+    spec = KVCacheSpec(Hkv, kv_dtype=cfg["kv"])
+    alloc = BlockAllocator(nb, bytes_per_block=spec.bytes_per_block)
+    alloc.pool._free = [int(x) for x in np.random.default_rng(7).permutation(nb)]  # random block ids, as the stationary bench
+    seqs = list(range(B))
+    slots0 = []
+    for b in seqs:
+        alloc.allocate(b)
+        slots0 += alloc.append_slots(b, int(lens[b]))
+    caches = [PagedKVCache(spec, nb, device=dev) for _ in range(layers)]
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(11)
+    sl_all = torch.tensor(slots0, dtype=torch.int32, device=dev)
+    for s0 in range(0, sl_all.numel(), 1 << 15):
+        sl = sl_all[s0: s0 + (1 << 15)]
+        kv = torch.randn((2, sl.numel(), Hkv, 128), device=dev, generator=gen)
+        kv = (kv * torch.exp(0.5 * torch.randn((2, sl.numel(), Hkv, 1), device=dev, generator=gen))).to(torch.bfloat16)
+        quantize_append(caches[0], kv[0], kv[1], sl)
+    del kv
+    for c in caches[1:]:
+        c.pool.copy_(caches[0].pool)
+    max_blocks = int(np.ceil((lens.max() + steps_total) / 16)) + 1
+    table = BlockTable(B, max_blocks, device=dev)
+    table.sync(alloc, seqs)
+    q = torch.randn((B, Hq, 128), device=dev, generator=gen).to(torch.bfloat16)
+    k_new = torch.randn((B, Hkv, 128), device=dev, generator=gen).to(torch.bfloat16)
+    v_new = torch.randn((B, Hkv, 128), device=dev, generator=gen).to(torch.bfloat16)
+    out = torch.empty((B, Hq, 128), dtype=torch.bfloat16, device=dev)
+    total_pages = int(np.ceil((lens + 1) / 16).sum())
+    pps = ops.pages_per_split(B, Hkv, total_pages, max_blocks)
+    ws = torch.zeros(ops.workspace_bytes(B, Hq, Hkv, -(-max_blocks // pps)), dtype=torch.uint8, device=dev)
+    compute = torch.cuda.current_stream(dev)
+    copy_stream = torch.cuda.Stream(dev)
+    slot_host = [torch.empty((B,), dtype=torch.int32, pin_memory=True) for _ in range(2)]
+    slot_dev = [torch.empty((B,), dtype=torch.int32, device=dev) for _ in range(2)]
+    slot_ev = [None, None]
+    legacy = args.table_sync == "legacy"
+
+    def layer_steps(slots_d):
+        for c in caches:
+            ops.decode_step(c, k_new, v_new, slots_d, q, table.table, table.seq_lens, out=out,
+                            pages_per_split=pps, workspace=ws, append_tail_only=True)
+
+    host_s, wait_s = [], []
+    step_graphs = [None, None]
+
+    def launch_layers(i):
+        if args.serving_graphs:   # one CUDA graph of all layers' launches per slot buffer
+            if step_graphs[i] is None:
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g, stream=torch.cuda.Stream(dev)):
+                    layer_steps(slot_dev[i])
+                step_graphs[i] = g
+            step_graphs[i].replay()
+        else:
+            layer_steps(slot_dev[i])
+
+    def model_step(t):
+        i = t % 2
+        w0 = time.perf_counter()
+        if legacy:
+            compute.synchronize()
+        if slot_ev[i] is not None:
+            slot_ev[i].synchronize()  # bounded run-ahead: this slot buffer's step (t - 2) is done
+        h0 = time.perf_counter()
+        new = alloc.append_one(seqs)
+        slot_host[i].numpy()[:] = new
+        with torch.cuda.stream(copy_stream):
+            slot_dev[i].copy_(slot_host[i], non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(copy_stream)
+        table.sync(alloc, seqs, copy_stream=copy_stream)
+        compute.wait_event(ev)
+        host_s.append(time.perf_counter() - h0)
+        wait_s.append(h0 - w0)
+        launch_layers(i)
+        slot_ev[i] = torch.cuda.Event()
+        slot_ev[i].record(compute)
+
+    for t in range(args.warmup):
+        model_step(t)
+    torch.cuda.synchronize()
+    host_s.clear()
+    wait_s.clear()
+    sampler = ClockSampler(0)
+    with sampler:
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        w0 = time.perf_counter()
+        e0.record()
+        for t in range(args.steps):
+            model_step(args.warmup + t)
+        e1.record()
+        launch_s = time.perf_counter() - w0
+        torch.cuda.synchronize()
+    ms_step = e0.elapsed_time(e1) / args.steps
+    # the same layers with no host work: one step's launches in a CUDA graph
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        layer_steps(slot_dev[0])
+    g.replay()
+    torch.cuda.synchronize()
+    d0, d1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    d0.record()
+    for _ in range(args.steps):
+        g.replay()
+    d1.record()
+    torch.cuda.synchronize()
+    ms_graph = d0.elapsed_time(d1) / args.steps
+    alloc.check_invariants()
+    attn_bytes, append_bytes = algorithmic_bytes(lens + args.warmup + args.steps // 2, Hq, Hkv, B)
+    line = {
+        "mode": "serving", "metric": METRIC, "value": B / (ms_step * 1e-3), "unit": "decoded tokens/s (model)",
+        "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "layers": layers,
+        "ms_per_model_step": ms_step, "ms_per_layer": ms_step / layers,
+        "graph_ms_per_model_step": ms_graph, "overhead_vs_graph": ms_step / ms_graph - 1,
+        "host_ms_per_step": 1e3 * statistics.mean(host_s),
+        "host_wait_ms_per_step": 1e3 * statistics.mean(wait_s),
+        "host_loop_ms_per_step": 1e3 * launch_s / args.steps,
+        "host_ahead": 1e3 * (launch_s - sum(wait_s)) / args.steps < ms_step,
+        "launch": "one CUDA graph of the layers' launches per step" if args.serving_graphs
+        else "ops.decode_step per layer (eager)",
+        "table_sync": "legacy (compute stream synchronized before each step's host work)" if legacy
+        else "async (pinned staging, copy stream, no host wait)",
+        "hbm_gbs_per_layer": (attn_bytes + append_bytes) / (ms_step / layers * 1e-3) / 1e9,
+        "dtype": cfg["kv"].replace("fp8_e4m3", "e4m3"), "data": "synthetic",
+        "config": {"workload": cfg["workload"] + f"; {layers} layers, one pool each (%.1f GB)"
+                   % (layers * caches[0].nbytes() / 1e9), "pages_per_split": pps,
+                   "step": "host: append_one + BlockTable.sync + slot upload; device: kvq_decode_step "
+                           "(K1 + PDL K2) per layer; sequences grow by one token per step; "
+                           "host_ms = append_one + sync + upload, host_wait_ms = waiting for the slot "
+                           "buffer of step t - 2 (bounded run-ahead)"},
+        "gpu_launches": 2 * layers * args.steps, "clocks": sampler.summary(),
+    }
+    print(json.dumps(line), flush=True)
 
 
 # ---------------------------------------------------------------------------
@@ -660,33 +852,39 @@ def run_c5(args, cfg):
         ops.decode_step(cache, kv_step[0], kv_step[1], slots_step, q, table, lens_d, out=out,
                         pages_per_split=pps, workspace=ws, append_tail_only=True)
 
+    from paper_2605_29639_b200.ops import profile_next_decode
+    spans = torch.zeros((max(args.steps, 1), 2), dtype=torch.int64, device=dev)
     k1(); k2(); step(); torch.cuda.synchronize()
-    graphs = []
-    for fn in (k1, k2, step):
-        g = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(g):
-            fn()
-        graphs.append(g)
-    g_k1, g_k2, g_step = graphs
-    for _ in range(args.warmup):
-        g_step.replay()
+    g_k1, g_warm, g_timed = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g_k1):
+        k1()
+    with torch.cuda.graph(g_warm):
+        for _ in range(args.warmup):
+            step()
+    with torch.cuda.graph(g_timed):   # K steps unrolled; each K2 records its own grid span
+        for i in range(args.steps):
+            profile_next_decode(spans[i])
+            step()
+    g_warm.replay()
+    spans[:, 0] = torch.iinfo(torch.int64).max
+    spans[:, 1] = 0
     torch.cuda.synchronize()
     sampler = ClockSampler(0)
     with sampler:
         t0 = torch.cuda.Event(enable_timing=True); t1 = torch.cuda.Event(enable_timing=True)
         t0.record()
-        for i in range(args.steps):
-            g_step.replay()
+        g_timed.replay()
         t1.record()
         torch.cuda.synchronize()
     ms_step = t0.elapsed_time(t1) / args.steps
-    # per-kernel breakdown (separate graphs, no PDL): K1 and K2 each bracketed by events
-    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
+    sp = spans.cpu().numpy()
+    k2_ms = float((sp[:, 1] - sp[:, 0]).mean()) / 1e6   # K2 inside the PDL step (overlaps K1's tail)
+    # K1 alone (its own graph, bracketed by events): the prefill-append rate
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(args.steps)]
     for i in range(args.steps):
-        ev[i][0].record(); g_k1.replay(); ev[i][1].record(); g_k2.replay(); ev[i][2].record()
+        ev[i][0].record(); g_k1.replay(); ev[i][1].record()
     torch.cuda.synchronize()
     k1_ms = statistics.mean(e[0].elapsed_time(e[1]) for e in ev)
-    k2_ms = statistics.mean(e[1].elapsed_time(e[2]) for e in ev)
 
     # quantisation error vs fp32 attention over the unquantised K/V (group 0),
     # with the stationary decode token included
@@ -702,10 +900,13 @@ def run_c5(args, cfg):
         o = out[b].float()
         errs.append(((o - ref).abs().max().item(), ((o - ref).abs().max() / ref.abs().max()).item()))
     attn_logical = int(ctx.sum()) * Hkv * 264 + B * Hq * 512 + total_pages * 4
-    attn_unique = (ngroups * cfg["prefix"] + int((ctx - cfg["prefix"]).sum())) * Hkv * 264
+    attn_unique_kv = (ngroups * cfg["prefix"] + int((ctx - cfg["prefix"]).sum())) * Hkv * 264
+    attn_unique = attn_unique_kv + B * Hq * 512 + total_pages * 4
     append_bytes = T * Hkv * (2 * 128 * 2 + 2 * 128 + 8) + 4 * T
     peak, peak_kind = measured_peak()
-    achieved = attn_logical / (k2_ms * 1e-3) / 1e9
+    # HBM roofline on the bytes that must come from DRAM: each shared prefix
+    # page once (the 8 sequences of a group re-read it from L2)
+    achieved = attn_unique / (k2_ms * 1e-3) / 1e9
     line = {
         "metric": METRIC, "value": B / (ms_step * 1e-3), "unit": "tokens/s", "n_gpus": 1,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
@@ -718,14 +919,19 @@ def run_c5(args, cfg):
         "k1_ms": k1_ms, "k2_ms": k2_ms,
         "append_gbs": append_bytes / (k1_ms * 1e-3) / 1e9,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": None, "kernel": "kvq::decode_kernel",
-                     "algorithmic_bytes_per_launch": attn_logical, "unique_kv_bytes": attn_unique,
+                     "frac": achieved / peak, "traffic": ncu_traffic("c5")[0], "kernel": "kvq::decode_kernel",
+                     "algorithmic_bytes_per_launch": attn_unique, "unique_kv_bytes": attn_unique_kv,
+                     "logical_bytes_per_launch": attn_logical,
+                     "logical_gbs": attn_logical / (k2_ms * 1e-3) / 1e9,
                      "avg_launch_ms": k2_ms, "peak_source": peak_kind,
-                     "note": "logical (per-sequence) bytes; prefix pages are shared, so DRAM bytes are lower"},
+                     "kernel_time": "grid span of every timed K2 inside the PDL step graph",
+                     "note": "achieved = unique bytes (each shared prefix page once, + q/O + table) / K2 time; "
+                             "logical_gbs counts every sequence's reads of its prefix"},
         "quant_error_vs_fp32_unquantized": {"max_abs": max(e[0] for e in errs),
                                             "max_rel_to_row_max": max(e[1] for e in errs),
                                             "sequences": len(errs)},
         "gpu_launches": 2 * args.steps, "clocks": sampler.summary(),
+        "build": {"src_hash": __import__("paper_2605_29639_b200._build", fromlist=["x"]).source_hash()},
     }
     print(json.dumps(line), flush=True)
 
@@ -738,8 +944,6 @@ def main(argv=None):
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--k2-sample-every", type=int, default=8,
-                    help="bracket every n-th step's K2 with CUDA events (the per-launch roofline sample)")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--pages-per-split", type=int, default=None,
                     help="override the split-KV geometry (default: kvq_decode_pages_per_split)")
@@ -749,6 +953,12 @@ def main(argv=None):
     ap.add_argument("--gather", default="peer", choices=["peer", "nccl"],
                     help="N > 1: fuse the KV-head output all-gather into K2 over peer memory (default) "
                          "or run NCCL all_gather_into_tensor after K2")
+    ap.add_argument("--serving", action="store_true",
+                    help="drive --layers layers per model step from the allocator + BlockTable (run_serving)")
+    ap.add_argument("--layers", type=int, default=32)
+    ap.add_argument("--serving-graphs", action="store_true",
+                    help="--serving: replay one CUDA graph of all layers' launches per model step")
+    ap.add_argument("--table-sync", default="async", choices=["async", "legacy"])
     ap.add_argument("--kv", default=None, choices=["int8", "fp8_e4m3"],
                     help="override the config's KV dtype (the C5 INT8 vs FP8 sweep)")
     args = ap.parse_args(argv)
@@ -758,7 +968,9 @@ def main(argv=None):
     if args.kv:
         cfg["kv"] = args.kv
         cfg["workload"] = cfg["workload"].replace("INT8", args.kv.upper()) + f" [{args.kv} KV]"
-    if args.config == "c5":
+    if args.serving:
+        run_serving(args, cfg)
+    elif args.config == "c5":
         if args.impl == "reference":
             raise SystemExit("--impl reference is defined on the headline config (c2)")
         run_c5(args, cfg)

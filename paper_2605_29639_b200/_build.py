@@ -49,6 +49,17 @@ def build_kernels(force: bool = False, verbose: bool = False) -> Path:
     return LIB_PATH
 
 
+def source_hash() -> str:
+    """Hash of everything that determines libkvq.so's code (CUDA sources, the
+    ABI header, the nvcc flags): ties an ncu capture to the build it measured."""
+    import hashlib
+    h = hashlib.sha256(" ".join(NVCC_FLAGS).encode())
+    for f in sorted(CSRC.glob("*.cu")) + sorted(CSRC.glob("*.cuh")) + [REPO / "include" / "kvq.h"]:
+        h.update(f.name.encode())
+        h.update(f.read_bytes())
+    return h.hexdigest()[:16]
+
+
 def build_oracle(force: bool = False) -> Path:
     src = [ORACLE_DIR / "kvq_oracle.c", ORACLE_DIR / "kvq_oracle.h"]
     if force or _stale(ORACLE_LIB, src):

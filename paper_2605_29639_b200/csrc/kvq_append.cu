@@ -3,6 +3,8 @@
 // (kvq_quant_append).  Rounding contract: DESIGN.md §3.
 #include "kvq_common.cuh"
 
+#include <algorithm>
+
 namespace kvq {
 
 // ---------------------------------------------------------------------------
@@ -264,6 +266,209 @@ __global__ void __launch_bounds__(K1_THREADS, 3) quant_append_kernel(  // 80 reg
 }
 
 // ---------------------------------------------------------------------------
+// K1 tile loop (large appends: chunked prefill).  Same tile work and rounding
+// as quant_append_kernel, but a persistent grid (2 CTAs per SM) walks the
+// (16-token, 4-head) tiles, and the NEXT tile's rows and slots are loaded into
+// registers before the current tile is quantized and stored, so every warp
+// keeps a tile of loads in flight through its compute and store phases (the
+// one-shot kernel ran 2.4 waves of short CTAs, each exposing its whole load
+// latency).  No CTA-wide barrier: every warp decides "whole page" itself from
+// the tile's 16 slots (L1 hits), and the page image of one head is built by
+// its own pair of warps, which meet at a named barrier before one of them
+// issues the TMA bulk store; images are double-buffered, so the store of tile
+// n reads its buffer while tile n + 1 fills the other.
+// ---------------------------------------------------------------------------
+constexpr int K1L_CTAS = 2;
+
+struct TileRows {
+  uint4 raw[2][2][2];  // [token][K|V][lo|hi 16 B]
+  int slot[2];         // slots of this group's two tokens
+  int s16;             // lanes 0..15: slot of tile token `lane` (whole-page test)
+};
+
+__device__ __forceinline__ void load_tile(const __nv_bfloat16* __restrict__ k, const __nv_bfloat16* __restrict__ v,
+                                          int64_t k_stride, int64_t v_stride, const int32_t* __restrict__ slots,
+                                          int T, int Hkv, int t0, int h, int pp, int j, int lane, TileRows& r) {
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const int t = t0 + 2 * pp + i;
+    const bool in = t < T && h < Hkv;
+#pragma unroll
+    for (int kv = 0; kv < 2; ++kv) {
+      const __nv_bfloat16* src = (kv ? v + (int64_t)t * v_stride : k + (int64_t)t * k_stride) + h * HD + 16 * j;
+      r.raw[i][kv][0] = in ? __ldg(reinterpret_cast<const uint4*>(src)) : make_uint4(0, 0, 0, 0);
+      r.raw[i][kv][1] = in ? __ldg(reinterpret_cast<const uint4*>(src + 8)) : make_uint4(0, 0, 0, 0);
+    }
+    r.slot[i] = t < T ? __ldg(slots + t) : -1;
+  }
+  r.s16 = (lane < 16 && t0 + lane < T) ? __ldg(slots + t0 + lane) : -1;
+}
+
+template <int KVD>
+__global__ void __launch_bounds__(K1_THREADS, K1L_CTAS) quant_append_loop_kernel(
+    const __nv_bfloat16* __restrict__ k, const __nv_bfloat16* __restrict__ v, int64_t k_stride,
+    int64_t v_stride, const int32_t* __restrict__ slots, int T, int Hkv,
+    uint8_t* __restrict__ pool, int64_t num_blocks, int HG, int ntiles) {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  __shared__ __align__(128) uint8_t img[2][K1_HEADS][PAGE];
+  const int lane = threadIdx.x & 31;
+  const int grp = threadIdx.x >> 3, j = threadIdx.x & 7;
+  const int hh = grp >> 3, pp = grp & 7;
+  const bool issuer = (threadIdx.x & 63) == 0;  // one thread of the warp pair that builds head hh's image
+  const float qmax = KVD == KVQ_FP8_E4M3 ? 448.0f : 127.0f;
+  int buf = 0;
+  TileRows cur;
+  int tile = blockIdx.x;
+  if (tile < ntiles) {
+    const int tt = tile / HG;
+    load_tile(k, v, k_stride, v_stride, slots, T, Hkv, tt * 16, (tile - tt * HG) * K1_HEADS + hh, pp, j, lane, cur);
+  }
+  for (; tile < ntiles; tile += gridDim.x) {
+    const int tt = tile / HG, h = (tile - tt * HG) * K1_HEADS + hh;
+    TileRows nxt;
+    const int next = tile + gridDim.x;
+    if (next < ntiles) {  // in flight while this tile is quantized and stored
+      const int nt = next / HG;
+      load_tile(k, v, k_stride, v_stride, slots, T, Hkv, nt * 16, (next - nt * HG) * K1_HEADS + hh, pp, j, lane,
+                nxt);
+    }
+    // Whole-page test (every warp alike): 16 in-range tokens with slots blk*16 + 0..15.
+    const int first = __shfl_sync(FULL, cur.s16, 0);
+    const bool whole = __all_sync(FULL, lane >= 16 || (cur.s16 >= 0 && cur.s16 == first + lane &&
+                                                       (first & 15) == 0 && (first >> 4) < num_blocks));
+    // ---- per-row amax over the 8 lanes (NaN-propagating for INT8: flags NaN rows)
+    float am[4];
+#pragma unroll
+    for (int rr = 0; rr < 4; ++rr) {
+      float x[16];
+      bf16x16(cur.raw[rr >> 1][rr & 1][0], cur.raw[rr >> 1][rr & 1][1], x);
+      float a = 0.0f;
+#pragma unroll
+      for (int e = 0; e < 16; ++e) a = KVD == KVQ_INT8 ? max_nan(a, fabsf(x[e])) : fmaxf(a, fabsf(x[e]));
+#pragma unroll
+      for (int o = 1; o < 8; o <<= 1) {
+        const float b = __shfl_xor_sync(FULL, a, o);
+        a = KVD == KVQ_INT8 ? max_nan(a, b) : fmaxf(a, b);
+      }
+      am[rr] = a;
+    }
+    bool nanrow[4] = {false, false, false, false};
+    if (KVD == KVQ_INT8 &&
+        __any_sync(FULL, am[0] != am[0] || am[1] != am[1] || am[2] != am[2] || am[3] != am[3])) {
+#pragma unroll
+      for (int rr = 0; rr < 4; ++rr) {  // rare: NaN-ignoring amax of the rows that hold NaN
+        nanrow[rr] = am[rr] != am[rr];
+        float x[16];
+        bf16x16(cur.raw[rr >> 1][rr & 1][0], cur.raw[rr >> 1][rr & 1][1], x);
+        float a = 0.0f;
+#pragma unroll
+        for (int e = 0; e < 16; ++e) a = fmaxf(a, fabsf(x[e]));
+#pragma unroll
+        for (int o = 1; o < 8; o <<= 1) a = fmaxf(a, __shfl_xor_sync(FULL, a, o));
+        if (nanrow[rr]) am[rr] = a;
+      }
+    }
+    // ---- one IEEE division per lane: lane j -> row j & 3, scale (j >= 4) or inverse (j < 4)
+    float dv;
+    {
+      const int rr = j & 3;
+      const float a = rr == 0 ? am[0] : rr == 1 ? am[1] : rr == 2 ? am[2] : am[3];
+      const bool is_scale = j >= 4;
+      dv = __fdiv_rn(is_scale ? a : qmax, is_scale ? qmax : a);
+      if (!is_scale && !(a > 0.0f)) dv = 0.0f;
+    }
+    float inv[4];
+#pragma unroll
+    for (int rr = 0; rr < 4; ++rr) inv[rr] = __shfl_sync(FULL, dv, (lane & ~7) | rr);
+    uint32_t code[2][2][4];
+#pragma unroll
+    for (int rr = 0; rr < 4; ++rr) {
+      float x[16];
+      bf16x16(cur.raw[rr >> 1][rr & 1][0], cur.raw[rr >> 1][rr & 1][1], x);
+      if constexpr (KVD == KVQ_FP8_E4M3) {
+        e4m3x16(x, inv[rr], code[rr >> 1][rr & 1]);
+      } else {
+        const bool fast = !nanrow[rr] && am[rr] < INFINITY && inv[rr] < INFINITY;  // uniform per group
+        if (fast) int8x16<true>(x, inv[rr], code[rr >> 1][rr & 1]);
+        else int8x16<false>(x, inv[rr], code[rr >> 1][rr & 1]);
+      }
+    }
+    uint32_t il[8];
+#pragma unroll
+    for (int w = 0; w < 4; ++w) {
+      il[2 * w] = __byte_perm(code[0][1][w], code[1][1][w], 0x5140);
+      il[2 * w + 1] = __byte_perm(code[0][1][w], code[1][1][w], 0x7362);
+    }
+    const int rs = j & 3, ts = rs >> 1;
+    if (whole) {
+      const uint32_t img_s = smem_u32(img[buf][hh]);
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        const int tok = 2 * pp + i, p = tok & 7;
+        const uint32_t kb = img_s + p * 256 + 16 * (j & 3) + (2 * (j >> 2) + (tok >> 3)) * 4;
+#pragma unroll
+        for (int w = 0; w < 4; ++w) sts32(kb + 64 * (w ^ i), code[i][0][w]);
+      }
+#pragma unroll
+      for (int half = 0; half < 2; ++half)
+        sts128(img_s + v_code_off(2 * pp, 16 * j + 8 * half),
+               make_uint4(il[4 * half], il[4 * half + 1], il[4 * half + 2], il[4 * half + 3]));
+      if (j >= 4) sts32(img_s + ((rs & 1) ? VS_OFF : KS_OFF) + 4 * (2 * pp + ts), __float_as_uint(dv));
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      // The issuer first waits until every earlier store has read its image (the
+      // one from this buffer was issued two whole tiles ago); past the barrier
+      // the pair may refill the other buffer.
+      if (issuer) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+      asm volatile("bar.sync %0, 64;" ::"r"(1 + hh) : "memory");
+      if (issuer && h < Hkv) {
+        uint8_t* dst = pool + ((int64_t)(first >> 4) * Hkv + h) * PAGE;
+        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(img_s), "n"(PAGE)
+                     : "memory");
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      }
+      buf ^= 1;
+    } else {
+      bool live[2];
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        live[i] = cur.slot[i] >= 0 && (cur.slot[i] >> 4) < num_blocks && h < Hkv;
+        if (cur.slot[i] >= 0 && (cur.slot[i] >> 4) >= num_blocks && j == 0 && hh == 0) flag_dev_err(KVQ_DERR_SLOT);
+      }
+      const bool pair_adj = live[0] && live[1] && (cur.slot[0] & 1) == 0 && cur.slot[1] == cur.slot[0] + 1;
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        if (!live[i]) continue;
+        const int tok = cur.slot[i] & 15;
+        uint8_t* page = pool + ((int64_t)(cur.slot[i] >> 4) * Hkv + h) * PAGE;
+#pragma unroll
+        for (int w = 0; w < 4; ++w)
+          *reinterpret_cast<uint32_t*>(page + k_code_off(tok, 16 * j + 4 * w)) = code[i][0][w];
+        if (!pair_adj) {
+#pragma unroll
+          for (int w = 0; w < 4; ++w)
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+              page[v_code_off(tok, 16 * j + 4 * w + e)] = (uint8_t)(code[i][1][w] >> (8 * e));
+        }
+        if (j >= 4 && ts == i)
+          *reinterpret_cast<float*>(page + ((rs & 1) ? VS_OFF : KS_OFF) + 4 * tok) = dv;
+      }
+      if (pair_adj) {
+        const int tok = cur.slot[0] & 15;
+        uint8_t* page = pool + ((int64_t)(cur.slot[0] >> 4) * Hkv + h) * PAGE;
+#pragma unroll
+        for (int half = 0; half < 2; ++half)
+          *reinterpret_cast<uint4*>(page + v_code_off(tok, 16 * j + 8 * half)) =
+              make_uint4(il[4 * half], il[4 * half + 1], il[4 * half + 2], il[4 * half + 3]);
+      }
+    }
+    cur = nxt;
+  }
+  // the images must stay valid until the bulk copies have read them
+  if (issuer) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+
+// ---------------------------------------------------------------------------
 // K1r: the decode-shaped append (a few tokens, each in a different page).
 // One warp per (token, head): lane l quantizes K and V elements [4l, 4l+4)
 // (one LDG.64 each), so the per-warp chain is ~100 instructions and a
@@ -346,6 +551,8 @@ int kvq_quant_append(const void* k, const void* v, int64_t k_token_stride, int64
   static const bool carve = [] {
     const void* fns[] = {(const void*)kvq::quant_append_kernel<KVQ_INT8>,
                          (const void*)kvq::quant_append_kernel<KVQ_FP8_E4M3>,
+                         (const void*)kvq::quant_append_loop_kernel<KVQ_INT8>,
+                         (const void*)kvq::quant_append_loop_kernel<KVQ_FP8_E4M3>,
                          (const void*)kvq::quant_append_rows_kernel<KVQ_INT8>,
                          (const void*)kvq::quant_append_rows_kernel<KVQ_FP8_E4M3>};
     for (const void* f : fns)
@@ -370,13 +577,17 @@ int kvq_quant_append(const void* k, const void* v, int64_t k_token_stride, int64
     return check_launch("quant_append");
   }
   const int HG = (Hkv + kvq::K1_HEADS - 1) / kvq::K1_HEADS;
-  const dim3 grid((unsigned)((T + 15) / 16), (unsigned)HG);
+  const int64_t ntiles = (int64_t)((T + 15) / 16) * HG;
+  if (ntiles > INT32_MAX) return fail(KVQ_EINVAL, "quant_append: too many tokens");
+  int sms = 148, dev = 0;
+  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const unsigned grid = (unsigned)std::min<int64_t>(ntiles, (int64_t)sms * kvq::K1L_CTAS);
   if (kv_dtype == KVQ_INT8)
-    kvq::quant_append_kernel<KVQ_INT8><<<grid, kvq::K1_THREADS, 0, st>>>(
-        kp, vp, k_token_stride, v_token_stride, slot_mapping, T, Hkv, pp, num_blocks);
+    kvq::quant_append_loop_kernel<KVQ_INT8><<<grid, kvq::K1_THREADS, 0, st>>>(
+        kp, vp, k_token_stride, v_token_stride, slot_mapping, T, Hkv, pp, num_blocks, HG, (int)ntiles);
   else
-    kvq::quant_append_kernel<KVQ_FP8_E4M3><<<grid, kvq::K1_THREADS, 0, st>>>(
-        kp, vp, k_token_stride, v_token_stride, slot_mapping, T, Hkv, pp, num_blocks);
+    kvq::quant_append_loop_kernel<KVQ_FP8_E4M3><<<grid, kvq::K1_THREADS, 0, st>>>(
+        kp, vp, k_token_stride, v_token_stride, slot_mapping, T, Hkv, pp, num_blocks, HG, (int)ntiles);
   return check_launch("quant_append");
 }
 

@@ -52,8 +52,22 @@ def main():
         e1.record()
         torch.cuda.synchronize()
         t = e0.elapsed_time(e1) / n
-        print(f"K1 {kv} {path or 'in-tree'}: T={T} x {Hkv} heads, {t * 1e3:.2f} us/launch, "
-              f"{byt / t / 1e6:.0f} GB/s algorithmic ({byt / 1e6:.1f} MB)")
+        # cold L2 (the serving case: the rows come from the QKV projection, the
+        # pages were last touched a step ago): a 256 MB memset before each launch
+        flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+        cold = []
+        for _ in range(20):
+            flush.zero_()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            ops.quantize_append(cache, k, v, sl)
+            b.record()
+            torch.cuda.synchronize()
+            cold.append(a.elapsed_time(b))
+        tc = sorted(cold)[len(cold) // 2]
+        print(f"K1 {kv} {path or 'in-tree'}: T={T} x {Hkv} heads, {t * 1e3:.2f} us/launch back to back "
+              f"({byt / t / 1e6:.0f} GB/s), {tc * 1e3:.2f} us cold-L2 median ({byt / tc / 1e6:.0f} GB/s) "
+              f"algorithmic ({byt / 1e6:.1f} MB)")
 
 
 if __name__ == "__main__":

@@ -3,31 +3,23 @@
 // (kvq_quant_append).  Rounding contract: DESIGN.md §3.
 #include "kvq_common.cuh"
 
+#include <cudaTypedefs.h>
+
 #include <algorithm>
 
 namespace kvq {
 
 // ---------------------------------------------------------------------------
-// K1: quantize-on-append.  CTA = 16 consecutive tokens x 4 kv heads; an
-// 8-lane group owns one (token pair 2p/2p+1, head): its 4 rows (K and V of
-// both tokens, 16 elements per lane) are loaded up front with LDG.128 and
-// their amax reduced over the 8 lanes.  Each lane then performs ONE of the
-// group's 8 IEEE divisions (the scale or the inverse of one row) and the
-// results are shuffled to where they are needed.  INT8 codes come from the
-// exact round-to-nearest-even of an fp32 add of 1.5 * 2^23 (|y| <= 127 lands
-// in the low mantissa byte) and byte permutes; rows holding NaN / inf, or
-// whose inverse overflows (subnormal amax), take the F2I path instead, so the
-// contract of DESIGN.md §3 holds bit for bit.  Output:
-//   * whole page (slots blk*16 + 0..15: chunked prefill): the page image is
-//     built in shared memory (st.shared, base + immediate offsets) and
-//     written by one TMA bulk store per (block, head);
-//   * otherwise (scattered tokens): direct global stores, V as interleaved
-//     16-byte chunks when the pair's two slots are adjacent, else byte-wise.
+// K1 quantizer math, per 8-lane group.  The group owns one (token pair, head):
+// its 4 rows (K and V of both tokens; lane j holds elements [16j, 16j+16) of
+// each) are in registers.  Each row's amax is reduced over the 8 lanes; each
+// lane then performs ONE of the group's 8 IEEE divisions (the scale or the
+// inverse of one row) and the results are shuffled to where they are needed.
+// INT8 codes come from the exact round-to-nearest-even of an fp32 add of
+// 1.5 * 2^23 (|y| <= 127 lands in the low mantissa byte) and byte permutes;
+// rows holding NaN / inf, or whose inverse overflows (subnormal amax), take the
+// F2I path instead, so the contract of DESIGN.md §3 holds bit for bit.
 // ---------------------------------------------------------------------------
-constexpr int K1_THREADS = 256;
-constexpr int K1_HEADS = 4;
-
-
 __device__ __forceinline__ float max_nan(float a, float b) {
   float d;
   asm("max.NaN.f32 %0, %1, %2;" : "=f"(d) : "f"(a), "f"(b));
@@ -85,50 +77,16 @@ __device__ __forceinline__ void sts128(uint32_t a, uint4 v) {
                : "memory");
 }
 
-template <int KVD>
-__global__ void __launch_bounds__(K1_THREADS, 3) quant_append_kernel(  // 80 regs, no spills
-    const __nv_bfloat16* __restrict__ k, const __nv_bfloat16* __restrict__ v, int64_t k_stride,
-    int64_t v_stride, const int32_t* __restrict__ slots, int T, int Hkv,
-    uint8_t* __restrict__ pool, int64_t num_blocks) {
-  // A K2 launched behind this kernel with programmatic serialization may start
-  // its prologue now; it waits (griddepcontrol.wait) before reading any page.
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-  __shared__ __align__(128) uint8_t img[K1_HEADS][PAGE];
-  const int t0 = blockIdx.x * 16, h0 = blockIdx.y * K1_HEADS;
-  const int lane = threadIdx.x & 31;
-  const int grp = threadIdx.x >> 3, j = threadIdx.x & 7;  // lane j of the group owns d [16j, 16j+16)
-  const int hh = grp >> 3, pp = grp & 7;                  // head h0+hh, tokens t0+2pp, t0+2pp+1
-  const int h = h0 + hh;
-  // Row loads first (they do not depend on the slots), then the slot loads.
-  uint4 raw[2][2][2];  // [token][K|V][lo|hi 16 B]
-#pragma unroll
-  for (int i = 0; i < 2; ++i) {
-    const int t = t0 + 2 * pp + i;
-    const bool in = t < T && h < Hkv;
-#pragma unroll
-    for (int kv = 0; kv < 2; ++kv) {
-      const __nv_bfloat16* src = (kv ? v + (int64_t)t * v_stride : k + (int64_t)t * k_stride) + h * HD + 16 * j;
-      raw[i][kv][0] = in ? __ldg(reinterpret_cast<const uint4*>(src)) : make_uint4(0, 0, 0, 0);
-      raw[i][kv][1] = in ? __ldg(reinterpret_cast<const uint4*>(src + 8)) : make_uint4(0, 0, 0, 0);
-    }
-  }
-  int slot[2];
-#pragma unroll
-  for (int i = 0; i < 2; ++i) {
-    const int t = t0 + 2 * pp + i;
-    slot[i] = t < T ? __ldg(slots + t) : -1;
-  }
-  // Whole-page test: 16 in-range tokens with slots blk*16 + 0..15.
-  int my_slot = -1;
-  if (threadIdx.x < 16 && t0 + threadIdx.x < T) my_slot = __ldg(slots + t0 + threadIdx.x);
-  const int first = t0 < T ? __ldg(slots + t0) : -1;
-  const bool mine_ok = threadIdx.x >= 16 ||
-                       (my_slot >= 0 && my_slot == first + (int)threadIdx.x && (first & 15) == 0 &&
-                        (first >> 4) < num_blocks);
-  const bool whole = __syncthreads_and(mine_ok);
+struct GroupCodes {
+  uint32_t kc[2][4];  // K codes of the pair's tokens 0 / 1 (this lane's 16 values)
+  uint32_t il[8];     // V codes of the pair, token-interleaved: bytes (d, t0), (d, t1), d = 16j .. 16j+15
+  float dv;           // this lane's division: row j & 3 (= 2 * token + kv), scale (j >= 4) or inverse
+};
 
-  // ---- per-row amax over the 8 lanes (NaN-propagating for INT8: flags NaN rows)
+template <int KVD>
+__device__ __forceinline__ void quant_group(const uint4 (&raw)[2][2][2], int lane, int j, GroupCodes& g) {
   const float qmax = KVD == KVQ_FP8_E4M3 ? 448.0f : 127.0f;
+  // ---- per-row amax over the 8 lanes (NaN-propagating for INT8: flags NaN rows)
   float am[4];  // row rr = 2 * token + kv
 #pragma unroll
   for (int rr = 0; rr < 4; ++rr) {
@@ -159,101 +117,85 @@ __global__ void __launch_bounds__(K1_THREADS, 3) quant_append_kernel(  // 80 reg
       if (nanrow[rr]) am[rr] = a;
     }
   }
-  // ---- one IEEE division per lane: lane j -> row j & 3, scale (j >= 4) or inverse (j < 4)
-  float dv;
+  // ---- one IEEE division per lane
   {
     const int rr = j & 3;
     const float a = rr == 0 ? am[0] : rr == 1 ? am[1] : rr == 2 ? am[2] : am[3];
     const bool is_scale = j >= 4;
-    dv = __fdiv_rn(is_scale ? a : qmax, is_scale ? qmax : a);
-    if (!is_scale && !(a > 0.0f)) dv = 0.0f;
+    g.dv = __fdiv_rn(is_scale ? a : qmax, is_scale ? qmax : a);
+    if (!is_scale && !(a > 0.0f)) g.dv = 0.0f;
   }
   float inv[4];
 #pragma unroll
-  for (int rr = 0; rr < 4; ++rr) inv[rr] = __shfl_sync(FULL, dv, (lane & ~7) | rr);
-
-  // ---- codes: [token][K|V][4 words]
-  uint32_t code[2][2][4];
+  for (int rr = 0; rr < 4; ++rr) inv[rr] = __shfl_sync(FULL, g.dv, (lane & ~7) | rr);
+  uint32_t vc[2][4];
 #pragma unroll
   for (int rr = 0; rr < 4; ++rr) {
     float x[16];
     bf16x16(raw[rr >> 1][rr & 1][0], raw[rr >> 1][rr & 1][1], x);
+    uint32_t(&c)[4] = (rr & 1) ? vc[rr >> 1] : g.kc[rr >> 1];
     if constexpr (KVD == KVQ_FP8_E4M3) {
-      e4m3x16(x, inv[rr], code[rr >> 1][rr & 1]);
+      e4m3x16(x, inv[rr], c);
     } else {
       const bool fast = !nanrow[rr] && am[rr] < INFINITY && inv[rr] < INFINITY;  // uniform per group
-      if (fast) int8x16<true>(x, inv[rr], code[rr >> 1][rr & 1]);
-      else int8x16<false>(x, inv[rr], code[rr >> 1][rr & 1]);
+      if (fast) int8x16<true>(x, inv[rr], c);
+      else int8x16<false>(x, inv[rr], c);
     }
   }
-  // V codes of the token pair interleaved: bytes (d, t0), (d, t1) for d = 16j .. 16j+15
-  // form logical pair-row bytes [32j, 32j+32) = two 16-byte chunks.
-  uint32_t il[8];
 #pragma unroll
   for (int w = 0; w < 4; ++w) {
-    il[2 * w] = __byte_perm(code[0][1][w], code[1][1][w], 0x5140);
-    il[2 * w + 1] = __byte_perm(code[0][1][w], code[1][1][w], 0x7362);
+    g.il[2 * w] = __byte_perm(vc[0][w], vc[1][w], 0x5140);
+    g.il[2 * w + 1] = __byte_perm(vc[0][w], vc[1][w], 0x7362);
   }
-  const int rs = j & 3, ts = rs >> 1;  // the scale this lane holds (j >= 4): row rs, token ts
+}
 
-  if (whole) {
-    // ---- page image in shared memory; K word w of token tok sits at
-    //      p*256 + 16c + (2*half + hi)*4 + 64*(w ^ (p & 1)), p = tok & 7 (p & 1 == i here)
-    const uint32_t img_s = smem_u32(img[hh]);
+// Page image of one head in shared memory (a whole block: tokens 2pp, 2pp + 1
+// of this group).  K word w of token tok sits at
+// p*256 + 16c + (2*half + hi)*4 + 64*(w ^ (p & 1)), p = tok & 7 (p & 1 == i here).
+__device__ __forceinline__ void write_image(uint32_t img_s, int pp, int j, const GroupCodes& g) {
 #pragma unroll
-    for (int i = 0; i < 2; ++i) {
-      const int tok = 2 * pp + i, p = tok & 7;
-      const uint32_t kb = img_s + p * 256 + 16 * (j & 3) + (2 * (j >> 2) + (tok >> 3)) * 4;
+  for (int i = 0; i < 2; ++i) {
+    const int tok = 2 * pp + i, p = tok & 7;
+    const uint32_t kb = img_s + p * 256 + 16 * (j & 3) + (2 * (j >> 2) + (tok >> 3)) * 4;
 #pragma unroll
-      for (int w = 0; w < 4; ++w) sts32(kb + 64 * (w ^ i), code[i][0][w]);
-    }
-#pragma unroll
-    for (int half = 0; half < 2; ++half)
-      sts128(img_s + v_code_off(2 * pp, 16 * j + 8 * half),
-             make_uint4(il[4 * half], il[4 * half + 1], il[4 * half + 2], il[4 * half + 3]));
-    if (j >= 4) sts32(img_s + ((rs & 1) ? VS_OFF : KS_OFF) + 4 * (2 * pp + ts), __float_as_uint(dv));
-    // generic-proxy smem writes -> visible to the bulk copy (async proxy)
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    __syncthreads();
-    const int nh = min(K1_HEADS, Hkv - h0);
-    if (threadIdx.x < nh) {
-      uint8_t* dst = pool + ((int64_t)(first >> 4) * Hkv + h0 + threadIdx.x) * PAGE;
-      asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst),
-                   "r"(smem_u32(img[threadIdx.x])), "n"(PAGE)
-                   : "memory");
-      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-      // Only the shared-memory reads must finish before the CTA exits (and its
-      // smem is reused); the global writes complete with the grid.
-      asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-    }
-    return;
+    for (int w = 0; w < 4; ++w) sts32(kb + 64 * (w ^ i), g.kc[i][w]);
   }
+#pragma unroll
+  for (int half = 0; half < 2; ++half)
+    sts128(img_s + v_code_off(2 * pp, 16 * j + 8 * half),
+           make_uint4(g.il[4 * half], g.il[4 * half + 1], g.il[4 * half + 2], g.il[4 * half + 3]));
+  const int rs = j & 3, ts = rs >> 1;
+  if (j >= 4) sts32(img_s + ((rs & 1) ? VS_OFF : KS_OFF) + 4 * (2 * pp + ts), __float_as_uint(g.dv));
+}
 
-  // ---- scattered tokens: direct global stores
+// Scattered tokens (not one whole block): direct global stores, V as
+// interleaved 16-byte chunks when the pair's two slots are adjacent, else byte-wise.
+__device__ __forceinline__ void store_scattered(uint8_t* __restrict__ pool, int64_t num_blocks, int Hkv, int h,
+                                                const int (&slot)[2], int j, bool flag_lane, const GroupCodes& g) {
   bool live[2];
 #pragma unroll
   for (int i = 0; i < 2; ++i) {
     live[i] = slot[i] >= 0 && (slot[i] >> 4) < num_blocks && h < Hkv;
-    if (slot[i] >= 0 && (slot[i] >> 4) >= num_blocks && j == 0 && hh == 0) flag_dev_err(KVQ_DERR_SLOT);
+    if (slot[i] >= 0 && (slot[i] >> 4) >= num_blocks && flag_lane) flag_dev_err(KVQ_DERR_SLOT);
   }
   const bool pair_adj = live[0] && live[1] && (slot[0] & 1) == 0 && slot[1] == slot[0] + 1;
+  const int rs = j & 3, ts = rs >> 1;
 #pragma unroll
   for (int i = 0; i < 2; ++i) {
     if (!live[i]) continue;
     const int tok = slot[i] & 15;
     uint8_t* page = pool + ((int64_t)(slot[i] >> 4) * Hkv + h) * PAGE;
 #pragma unroll
-    for (int w = 0; w < 4; ++w)
-      *reinterpret_cast<uint32_t*>(page + k_code_off(tok, 16 * j + 4 * w)) = code[i][0][w];
+    for (int w = 0; w < 4; ++w) *reinterpret_cast<uint32_t*>(page + k_code_off(tok, 16 * j + 4 * w)) = g.kc[i][w];
     if (!pair_adj) {  // lone token: V bytes at 2d + (tok & 1)
 #pragma unroll
-      for (int w = 0; w < 4; ++w)
+      for (int w = 0; w < 4; ++w) {
+        const uint32_t vw = __byte_perm(g.il[2 * w], g.il[2 * w + 1], i ? 0x7531 : 0x6420);
 #pragma unroll
-        for (int e = 0; e < 4; ++e)
-          page[v_code_off(tok, 16 * j + 4 * w + e)] = (uint8_t)(code[i][1][w] >> (8 * e));
+        for (int e = 0; e < 4; ++e) page[v_code_off(tok, 16 * j + 4 * w + e)] = (uint8_t)(vw >> (8 * e));
+      }
     }
-    if (j >= 4 && ts == i)
-      *reinterpret_cast<float*>(page + ((rs & 1) ? VS_OFF : KS_OFF) + 4 * tok) = dv;
+    if (j >= 4 && ts == i) *reinterpret_cast<float*>(page + ((rs & 1) ? VS_OFF : KS_OFF) + 4 * tok) = g.dv;
   }
   if (pair_adj) {
     const int tok = slot[0] & 15;  // even
@@ -261,166 +203,148 @@ __global__ void __launch_bounds__(K1_THREADS, 3) quant_append_kernel(  // 80 reg
 #pragma unroll
     for (int half = 0; half < 2; ++half)
       *reinterpret_cast<uint4*>(page + v_code_off(tok, 16 * j + 8 * half)) =
-          make_uint4(il[4 * half], il[4 * half + 1], il[4 * half + 2], il[4 * half + 3]);
+          make_uint4(g.il[4 * half], g.il[4 * half + 1], g.il[4 * half + 2], g.il[4 * half + 3]);
   }
 }
 
 // ---------------------------------------------------------------------------
-// K1 tile loop (large appends: chunked prefill).  Same tile work and rounding
-// as quant_append_kernel, but a persistent grid (2 CTAs per SM) walks the
-// (16-token, 4-head) tiles, and the NEXT tile's rows and slots are loaded into
-// registers before the current tile is quantized and stored, so every warp
-// keeps a tile of loads in flight through its compute and store phases (the
-// one-shot kernel ran 2.4 waves of short CTAs, each exposing its whole load
-// latency).  No CTA-wide barrier: every warp decides "whole page" itself from
-// the tile's 16 slots (L1 hits), and the page image of one head is built by
-// its own pair of warps, which meet at a named barrier before one of them
-// issues the TMA bulk store; images are double-buffered, so the store of tile
-// n reads its buffer while tile n + 1 fills the other.
+// K1 tile kernel (large appends: chunked prefill, T * Hkv > K1_ROWS_MAX).
+// Work unit = 16 consecutive tokens x 1 kv head (one page when the 16 slots
+// are one whole block).  Persistent grid, 2 CTAs per SM, 9 warps:
+//   * warp 0, the producer: one thread issues, per unit, two TMA tensor loads
+//     (cp.async.bulk.tensor.2d over the [T][Hkv * 128] bf16 K and V views,
+//     box 16 tokens x 128 = 4 KB each; tokens past T are zero-filled) into a
+//     ring of K1T_STAGES 8 KB stages; the stage's mbarrier counts the bytes;
+//   * warps 1..8, four teams of 2 consumers: team i & 3 quantizes the CTA's
+//     i-th unit.  An 8-lane group owns one token pair and reads its 4 rows (K
+//     and V of both tokens) from the stage, two LDS.128 per row; each warp
+//     releases the stage (one mbarrier arrive) as soon as its rows are in
+//     registers;
+//   * whole page: the team builds the page image in shared memory (double-
+//     buffered), meets at a named barrier, and one thread issues a 4224-byte
+//     TMA bulk store; otherwise direct global stores.
+// The ring keeps up to 8 x 8 KB of row loads in flight per CTA whatever the
+// consumers are doing.  Designs measured before it (profiles/r2/k1_*):
+// register prefetch of one tile per warp (0.47 of the copy peak, LDG
+// long-scoreboard stalls); per-row 512-byte cp.async.bulk copies (32 per unit:
+// the producer's serialized issue loop, ~86 cycles per copy, was the
+// bottleneck); 2-head units (7.1 per CTA on C5, so 1 CTA in 7 ran an 8th unit
+// after the others were done: a 2-3 us tail in the per-CTA timeline).
 // ---------------------------------------------------------------------------
-constexpr int K1L_CTAS = 2;
+constexpr int K1T_STAGES = 8;
+constexpr int K1T_STAGE = 2 * 16 * HD * 2;       // K|V x 16 tokens x 256 B
+constexpr int K1T_TEAMS = 4;                     // of 2 warps
+constexpr int K1T_THREADS = 32 + K1T_TEAMS * 64;
+constexpr int K1T_IMG = K1T_TEAMS * 2 * PAGE;    // [team][buf] page images
+constexpr int K1T_SMEM = K1T_STAGES * K1T_STAGE + K1T_IMG + 2 * K1T_STAGES * 8 + 128;  // + alignment slack
 
-struct TileRows {
-  uint4 raw[2][2][2];  // [token][K|V][lo|hi 16 B]
-  int slot[2];         // slots of this group's two tokens
-  int s16;             // lanes 0..15: slot of tile token `lane` (whole-page test)
+// TMA tensor load of one box into shared memory, completion on an mbarrier.
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar,
+                                            uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
+
+struct UnitSlots {
+  int slot[2];  // slots of this group's two tokens
+  int s16;      // lanes 0..15: slot of unit token `lane` (whole-page test)
 };
-
-__device__ __forceinline__ void load_tile(const __nv_bfloat16* __restrict__ k, const __nv_bfloat16* __restrict__ v,
-                                          int64_t k_stride, int64_t v_stride, const int32_t* __restrict__ slots,
-                                          int T, int Hkv, int t0, int h, int pp, int j, int lane, TileRows& r) {
+__device__ __forceinline__ void load_slots(const int32_t* __restrict__ slots, int T, int t0, int pp, int lane,
+                                           UnitSlots& s) {
 #pragma unroll
-  for (int i = 0; i < 2; ++i) {
-    const int t = t0 + 2 * pp + i;
-    const bool in = t < T && h < Hkv;
-#pragma unroll
-    for (int kv = 0; kv < 2; ++kv) {
-      const __nv_bfloat16* src = (kv ? v + (int64_t)t * v_stride : k + (int64_t)t * k_stride) + h * HD + 16 * j;
-      r.raw[i][kv][0] = in ? __ldg(reinterpret_cast<const uint4*>(src)) : make_uint4(0, 0, 0, 0);
-      r.raw[i][kv][1] = in ? __ldg(reinterpret_cast<const uint4*>(src + 8)) : make_uint4(0, 0, 0, 0);
-    }
-    r.slot[i] = t < T ? __ldg(slots + t) : -1;
-  }
-  r.s16 = (lane < 16 && t0 + lane < T) ? __ldg(slots + t0 + lane) : -1;
+  for (int i = 0; i < 2; ++i) s.slot[i] = t0 + 2 * pp + i < T ? __ldg(slots + t0 + 2 * pp + i) : -1;
+  s.s16 = (lane < 16 && t0 + lane < T) ? __ldg(slots + t0 + lane) : -1;
 }
 
 template <int KVD>
-__global__ void __launch_bounds__(K1_THREADS, K1L_CTAS) quant_append_loop_kernel(
-    const __nv_bfloat16* __restrict__ k, const __nv_bfloat16* __restrict__ v, int64_t k_stride,
-    int64_t v_stride, const int32_t* __restrict__ slots, int T, int Hkv,
-    uint8_t* __restrict__ pool, int64_t num_blocks, int HG, int ntiles) {
+__global__ void __launch_bounds__(K1T_THREADS, 2) quant_append_tile_kernel(
+    const __grid_constant__ CUtensorMap tmk, const __grid_constant__ CUtensorMap tmv,
+    const int32_t* __restrict__ slots, int T, int Hkv, uint8_t* __restrict__ pool, int64_t num_blocks,
+    int nunits) {
+  // A K2 launched behind this kernel with programmatic serialization may start
+  // its prologue now; it waits (griddepcontrol.wait) before reading any page.
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-  __shared__ __align__(128) uint8_t img[2][K1_HEADS][PAGE];
-  const int lane = threadIdx.x & 31;
-  const int grp = threadIdx.x >> 3, j = threadIdx.x & 7;
-  const int hh = grp >> 3, pp = grp & 7;
-  const bool issuer = (threadIdx.x & 63) == 0;  // one thread of the warp pair that builds head hh's image
-  const float qmax = KVD == KVQ_FP8_E4M3 ? 448.0f : 127.0f;
-  int buf = 0;
-  TileRows cur;
-  int tile = blockIdx.x;
-  if (tile < ntiles) {
-    const int tt = tile / HG;
-    load_tile(k, v, k_stride, v_stride, slots, T, Hkv, tt * 16, (tile - tt * HG) * K1_HEADS + hh, pp, j, lane, cur);
-  }
-  for (; tile < ntiles; tile += gridDim.x) {
-    const int tt = tile / HG, h = (tile - tt * HG) * K1_HEADS + hh;
-    TileRows nxt;
-    const int next = tile + gridDim.x;
-    if (next < ntiles) {  // in flight while this tile is quantized and stored
-      const int nt = next / HG;
-      load_tile(k, v, k_stride, v_stride, slots, T, Hkv, nt * 16, (next - nt * HG) * K1_HEADS + hh, pp, j, lane,
-                nxt);
+  extern __shared__ __align__(128) uint8_t smem_raw[];
+  uint8_t* const smem = smem_raw + ((128 - (smem_u32(smem_raw) & 127)) & 127);  // TMA boxes: 128-byte aligned
+  uint8_t* const stage = smem;
+  uint8_t* const imgs = smem + K1T_STAGES * K1T_STAGE;
+  uint64_t* const full = reinterpret_cast<uint64_t*>(imgs + K1T_IMG);
+  uint64_t* const empty = full + K1T_STAGES;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmk)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmv)) : "memory");
+    for (int s = 0; s < K1T_STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 2);  // one arrive per consumer warp of the team
     }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  if (warp == 0) {  // ---- producer
+    if (lane != 0) return;
+    const uint64_t pol = policy_evict_first();  // the rows are read once
+    int i = 0;
+    for (int u = blockIdx.x; u < nunits; u += gridDim.x, ++i) {
+      const int s = i % K1T_STAGES, r = i / K1T_STAGES;
+      if (r > 0) mbar_wait(&empty[s], (r - 1) & 1);
+      const int tt = u / Hkv, h = u - tt * Hkv;
+      mbar_arrive_expect_tx(&full[s], K1T_STAGE);  // full boxes, OOB elements included
+      tma_load_2d(stage + s * K1T_STAGE, &tmk, h * HD, tt * 16, &full[s], pol);
+      tma_load_2d(stage + s * K1T_STAGE + K1T_STAGE / 2, &tmv, h * HD, tt * 16, &full[s], pol);
+    }
+    return;
+  }
+
+  // ---- consumers
+  const int ct = threadIdx.x - 32, team = ct >> 6, tt_ = ct & 63;
+  const int pp = tt_ >> 3, j = lane & 7;  // tokens 2pp, 2pp + 1 of the unit; lane j of the group
+  const bool issuer = tt_ == 0;
+  uint8_t* const my_img = imgs + team * 2 * PAGE;  // + buf * PAGE
+  int buf = 0, i = team;
+  int u = blockIdx.x + team * gridDim.x;
+  UnitSlots cur;
+  if (u < nunits) load_slots(slots, T, (u / Hkv) * 16, pp, lane, cur);
+  for (; u < nunits; u += K1T_TEAMS * gridDim.x, i += K1T_TEAMS) {
+    const int tt = u / Hkv, h = u - tt * Hkv;
+    UnitSlots nxt;
+    const int un = u + K1T_TEAMS * gridDim.x;
+    if (un < nunits) load_slots(slots, T, (un / Hkv) * 16, pp, lane, nxt);  // in flight through this unit
+    const int s = i % K1T_STAGES;
+    mbar_wait(&full[s], (i / K1T_STAGES) & 1);
+    uint4 raw[2][2][2];  // [token][K|V][lo|hi 16 B]; tokens past T were zero-filled by the TMA
+    const uint8_t* sb = stage + s * K1T_STAGE + 32 * j;
+#pragma unroll
+    for (int i2 = 0; i2 < 2; ++i2)
+#pragma unroll
+      for (int kv = 0; kv < 2; ++kv) {
+        const uint8_t* rp = sb + kv * (K1T_STAGE / 2) + (2 * pp + i2) * (HD * 2);
+        raw[i2][kv][0] = lds128(rp);
+        raw[i2][kv][1] = lds128(rp + 16);
+      }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
     // Whole-page test (every warp alike): 16 in-range tokens with slots blk*16 + 0..15.
     const int first = __shfl_sync(FULL, cur.s16, 0);
     const bool whole = __all_sync(FULL, lane >= 16 || (cur.s16 >= 0 && cur.s16 == first + lane &&
                                                        (first & 15) == 0 && (first >> 4) < num_blocks));
-    // ---- per-row amax over the 8 lanes (NaN-propagating for INT8: flags NaN rows)
-    float am[4];
-#pragma unroll
-    for (int rr = 0; rr < 4; ++rr) {
-      float x[16];
-      bf16x16(cur.raw[rr >> 1][rr & 1][0], cur.raw[rr >> 1][rr & 1][1], x);
-      float a = 0.0f;
-#pragma unroll
-      for (int e = 0; e < 16; ++e) a = KVD == KVQ_INT8 ? max_nan(a, fabsf(x[e])) : fmaxf(a, fabsf(x[e]));
-#pragma unroll
-      for (int o = 1; o < 8; o <<= 1) {
-        const float b = __shfl_xor_sync(FULL, a, o);
-        a = KVD == KVQ_INT8 ? max_nan(a, b) : fmaxf(a, b);
-      }
-      am[rr] = a;
-    }
-    bool nanrow[4] = {false, false, false, false};
-    if (KVD == KVQ_INT8 &&
-        __any_sync(FULL, am[0] != am[0] || am[1] != am[1] || am[2] != am[2] || am[3] != am[3])) {
-#pragma unroll
-      for (int rr = 0; rr < 4; ++rr) {  // rare: NaN-ignoring amax of the rows that hold NaN
-        nanrow[rr] = am[rr] != am[rr];
-        float x[16];
-        bf16x16(cur.raw[rr >> 1][rr & 1][0], cur.raw[rr >> 1][rr & 1][1], x);
-        float a = 0.0f;
-#pragma unroll
-        for (int e = 0; e < 16; ++e) a = fmaxf(a, fabsf(x[e]));
-#pragma unroll
-        for (int o = 1; o < 8; o <<= 1) a = fmaxf(a, __shfl_xor_sync(FULL, a, o));
-        if (nanrow[rr]) am[rr] = a;
-      }
-    }
-    // ---- one IEEE division per lane: lane j -> row j & 3, scale (j >= 4) or inverse (j < 4)
-    float dv;
-    {
-      const int rr = j & 3;
-      const float a = rr == 0 ? am[0] : rr == 1 ? am[1] : rr == 2 ? am[2] : am[3];
-      const bool is_scale = j >= 4;
-      dv = __fdiv_rn(is_scale ? a : qmax, is_scale ? qmax : a);
-      if (!is_scale && !(a > 0.0f)) dv = 0.0f;
-    }
-    float inv[4];
-#pragma unroll
-    for (int rr = 0; rr < 4; ++rr) inv[rr] = __shfl_sync(FULL, dv, (lane & ~7) | rr);
-    uint32_t code[2][2][4];
-#pragma unroll
-    for (int rr = 0; rr < 4; ++rr) {
-      float x[16];
-      bf16x16(cur.raw[rr >> 1][rr & 1][0], cur.raw[rr >> 1][rr & 1][1], x);
-      if constexpr (KVD == KVQ_FP8_E4M3) {
-        e4m3x16(x, inv[rr], code[rr >> 1][rr & 1]);
-      } else {
-        const bool fast = !nanrow[rr] && am[rr] < INFINITY && inv[rr] < INFINITY;  // uniform per group
-        if (fast) int8x16<true>(x, inv[rr], code[rr >> 1][rr & 1]);
-        else int8x16<false>(x, inv[rr], code[rr >> 1][rr & 1]);
-      }
-    }
-    uint32_t il[8];
-#pragma unroll
-    for (int w = 0; w < 4; ++w) {
-      il[2 * w] = __byte_perm(code[0][1][w], code[1][1][w], 0x5140);
-      il[2 * w + 1] = __byte_perm(code[0][1][w], code[1][1][w], 0x7362);
-    }
-    const int rs = j & 3, ts = rs >> 1;
+    GroupCodes g;
+    quant_group<KVD>(raw, lane, j, g);
     if (whole) {
-      const uint32_t img_s = smem_u32(img[buf][hh]);
-#pragma unroll
-      for (int i = 0; i < 2; ++i) {
-        const int tok = 2 * pp + i, p = tok & 7;
-        const uint32_t kb = img_s + p * 256 + 16 * (j & 3) + (2 * (j >> 2) + (tok >> 3)) * 4;
-#pragma unroll
-        for (int w = 0; w < 4; ++w) sts32(kb + 64 * (w ^ i), code[i][0][w]);
-      }
-#pragma unroll
-      for (int half = 0; half < 2; ++half)
-        sts128(img_s + v_code_off(2 * pp, 16 * j + 8 * half),
-               make_uint4(il[4 * half], il[4 * half + 1], il[4 * half + 2], il[4 * half + 3]));
-      if (j >= 4) sts32(img_s + ((rs & 1) ? VS_OFF : KS_OFF) + 4 * (2 * pp + ts), __float_as_uint(dv));
+      const uint32_t img_s = smem_u32(my_img + buf * PAGE);
+      write_image(img_s, pp, j, g);
+      // generic-proxy smem writes -> visible to the bulk copy (async proxy)
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      // The issuer first waits until every earlier store has read its image (the
-      // one from this buffer was issued two whole tiles ago); past the barrier
-      // the pair may refill the other buffer.
+      // The issuer first waits until its earlier stores have read their images
+      // (the one from this buffer was issued two units ago); past the barrier
+      // the team may refill the other buffer.
       if (issuer) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-      asm volatile("bar.sync %0, 64;" ::"r"(1 + hh) : "memory");
-      if (issuer && h < Hkv) {
+      asm volatile("bar.sync %0, 64;" ::"r"(1 + team) : "memory");
+      if (issuer) {
         uint8_t* dst = pool + ((int64_t)(first >> 4) * Hkv + h) * PAGE;
         asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(img_s), "n"(PAGE)
                      : "memory");
@@ -428,39 +352,7 @@ __global__ void __launch_bounds__(K1_THREADS, K1L_CTAS) quant_append_loop_kernel
       }
       buf ^= 1;
     } else {
-      bool live[2];
-#pragma unroll
-      for (int i = 0; i < 2; ++i) {
-        live[i] = cur.slot[i] >= 0 && (cur.slot[i] >> 4) < num_blocks && h < Hkv;
-        if (cur.slot[i] >= 0 && (cur.slot[i] >> 4) >= num_blocks && j == 0 && hh == 0) flag_dev_err(KVQ_DERR_SLOT);
-      }
-      const bool pair_adj = live[0] && live[1] && (cur.slot[0] & 1) == 0 && cur.slot[1] == cur.slot[0] + 1;
-#pragma unroll
-      for (int i = 0; i < 2; ++i) {
-        if (!live[i]) continue;
-        const int tok = cur.slot[i] & 15;
-        uint8_t* page = pool + ((int64_t)(cur.slot[i] >> 4) * Hkv + h) * PAGE;
-#pragma unroll
-        for (int w = 0; w < 4; ++w)
-          *reinterpret_cast<uint32_t*>(page + k_code_off(tok, 16 * j + 4 * w)) = code[i][0][w];
-        if (!pair_adj) {
-#pragma unroll
-          for (int w = 0; w < 4; ++w)
-#pragma unroll
-            for (int e = 0; e < 4; ++e)
-              page[v_code_off(tok, 16 * j + 4 * w + e)] = (uint8_t)(code[i][1][w] >> (8 * e));
-        }
-        if (j >= 4 && ts == i)
-          *reinterpret_cast<float*>(page + ((rs & 1) ? VS_OFF : KS_OFF) + 4 * tok) = dv;
-      }
-      if (pair_adj) {
-        const int tok = cur.slot[0] & 15;
-        uint8_t* page = pool + ((int64_t)(cur.slot[0] >> 4) * Hkv + h) * PAGE;
-#pragma unroll
-        for (int half = 0; half < 2; ++half)
-          *reinterpret_cast<uint4*>(page + v_code_off(tok, 16 * j + 8 * half)) =
-              make_uint4(il[4 * half], il[4 * half + 1], il[4 * half + 2], il[4 * half + 3]);
-      }
+      store_scattered(pool, num_blocks, Hkv, h, cur.slot, j, j == 0, g);
     }
     cur = nxt;
   }
@@ -549,14 +441,14 @@ int kvq_quant_append(const void* k, const void* v, int64_t k_token_stride, int64
   // Same (max-shared) L1/smem carveout as K2 so a decode step never pays an
   // SM reconfiguration between the append and the attention kernel.
   static const bool carve = [] {
-    const void* fns[] = {(const void*)kvq::quant_append_kernel<KVQ_INT8>,
-                         (const void*)kvq::quant_append_kernel<KVQ_FP8_E4M3>,
-                         (const void*)kvq::quant_append_loop_kernel<KVQ_INT8>,
-                         (const void*)kvq::quant_append_loop_kernel<KVQ_FP8_E4M3>,
+    const void* fns[] = {(const void*)kvq::quant_append_tile_kernel<KVQ_INT8>,
+                         (const void*)kvq::quant_append_tile_kernel<KVQ_FP8_E4M3>,
                          (const void*)kvq::quant_append_rows_kernel<KVQ_INT8>,
                          (const void*)kvq::quant_append_rows_kernel<KVQ_FP8_E4M3>};
     for (const void* f : fns)
       cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
+    for (int i = 0; i < 2; ++i)
+      cudaFuncSetAttribute(fns[i], cudaFuncAttributeMaxDynamicSharedMemorySize, kvq::K1T_SMEM);
     return true;
   }();
   (void)carve;
@@ -576,18 +468,39 @@ int kvq_quant_append(const void* k, const void* v, int64_t k_token_stride, int64
           kp, vp, k_token_stride, v_token_stride, slot_mapping, T, Hkv, pp, num_blocks);
     return check_launch("quant_append");
   }
-  const int HG = (Hkv + kvq::K1_HEADS - 1) / kvq::K1_HEADS;
-  const int64_t ntiles = (int64_t)((T + 15) / 16) * HG;
-  if (ntiles > INT32_MAX) return fail(KVQ_EINVAL, "quant_append: too many tokens");
+  // Tile kernel: the rows are fetched by TMA tensor loads through two maps
+  // over the [T][Hkv][128] K and V views (16-byte aligned rows, checked above).
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = [] {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      fn = nullptr;
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }();
+  if (!encode) return fail(KVQ_ECUDA, "quant_append: cuTensorMapEncodeTiled unavailable");
+  CUtensorMap maps[2];
+  for (int m = 0; m < 2; ++m) {  // 2-D view [T][Hkv * 128]: box = 16 tokens x one head
+    const cuuint64_t dims[2] = {(cuuint64_t)kvq::HD * Hkv, (cuuint64_t)T};
+    const cuuint64_t strides[1] = {(cuuint64_t)(m ? v_token_stride : k_token_stride) * 2};
+    const cuuint32_t box[2] = {(cuuint32_t)kvq::HD, 16};
+    const cuuint32_t estr[2] = {1, 1};
+    const CUresult r = encode(&maps[m], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(m ? v : k), dims,
+                              strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(KVQ_EINVAL, "quant_append: cannot describe the k/v rows to the TMA");
+  }
+  const int64_t nunits = (int64_t)((T + 15) / 16) * Hkv;
+  if (nunits > INT32_MAX) return fail(KVQ_EINVAL, "quant_append: too many tokens");
   int sms = 148, dev = 0;
   if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const unsigned grid = (unsigned)std::min<int64_t>(ntiles, (int64_t)sms * kvq::K1L_CTAS);
+  const unsigned grid = (unsigned)std::min<int64_t>(nunits, (int64_t)sms * 2);
   if (kv_dtype == KVQ_INT8)
-    kvq::quant_append_loop_kernel<KVQ_INT8><<<grid, kvq::K1_THREADS, 0, st>>>(
-        kp, vp, k_token_stride, v_token_stride, slot_mapping, T, Hkv, pp, num_blocks, HG, (int)ntiles);
+    kvq::quant_append_tile_kernel<KVQ_INT8><<<grid, kvq::K1T_THREADS, kvq::K1T_SMEM, st>>>(
+        maps[0], maps[1], slot_mapping, T, Hkv, pp, num_blocks, (int)nunits);
   else
-    kvq::quant_append_loop_kernel<KVQ_FP8_E4M3><<<grid, kvq::K1_THREADS, 0, st>>>(
-        kp, vp, k_token_stride, v_token_stride, slot_mapping, T, Hkv, pp, num_blocks, HG, (int)ntiles);
+    kvq::quant_append_tile_kernel<KVQ_FP8_E4M3><<<grid, kvq::K1T_THREADS, kvq::K1T_SMEM, st>>>(
+        maps[0], maps[1], slot_mapping, T, Hkv, pp, num_blocks, (int)nunits);
   return check_launch("quant_append");
 }
 

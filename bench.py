@@ -852,11 +852,15 @@ def run_c5(args, cfg):
         ops.decode_step(cache, kv_step[0], kv_step[1], slots_step, q, table, lens_d, out=out,
                         pages_per_split=pps, workspace=ws, append_tail_only=True)
 
-    from paper_2605_29639_b200.ops import profile_next_decode
+    from paper_2605_29639_b200.ops import profile_next_append, profile_next_decode
     spans = torch.zeros((max(args.steps, 1), 2), dtype=torch.int64, device=dev)
+    k1_step_spans = torch.zeros_like(spans)   # K1 inside the timed step graph
+    k1_spans = torch.zeros_like(spans)        # K1 alone, one launch per graph replay
     k1(); k2(); step(); torch.cuda.synchronize()
     g_k1, g_warm, g_timed = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
+    k1_span_slot = torch.zeros(2, dtype=torch.int64, device=dev)
     with torch.cuda.graph(g_k1):
+        profile_next_append(k1_span_slot)
         k1()
     with torch.cuda.graph(g_warm):
         for _ in range(args.warmup):
@@ -864,10 +868,12 @@ def run_c5(args, cfg):
     with torch.cuda.graph(g_timed):   # K steps unrolled; each K2 records its own grid span
         for i in range(args.steps):
             profile_next_decode(spans[i])
+            profile_next_append(k1_step_spans[i])
             step()
     g_warm.replay()
-    spans[:, 0] = torch.iinfo(torch.int64).max
-    spans[:, 1] = 0
+    for sp_ in (spans, k1_step_spans):
+        sp_[:, 0] = torch.iinfo(torch.int64).max
+        sp_[:, 1] = 0
     torch.cuda.synchronize()
     sampler = ClockSampler(0)
     with sampler:
@@ -879,12 +885,19 @@ def run_c5(args, cfg):
     ms_step = t0.elapsed_time(t1) / args.steps
     sp = spans.cpu().numpy()
     k2_ms = float((sp[:, 1] - sp[:, 0]).mean()) / 1e6   # K2 inside the PDL step (overlaps K1's tail)
-    # K1 alone (its own graph, bracketed by events): the prefill-append rate
+    k1_step_ms = float((k1_step_spans[:, 1] - k1_step_spans[:, 0]).float().mean()) / 1e6
+    # K1 alone (its own graph, replayed back to back, bracketed by events; and
+    # its grid span, copied out of the graph's span slot after every replay):
+    # the prefill-append rate
     ev = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(args.steps)]
     for i in range(args.steps):
+        k1_span_slot[0] = torch.iinfo(torch.int64).max
+        k1_span_slot[1] = 0
         ev[i][0].record(); g_k1.replay(); ev[i][1].record()
+        k1_spans[i].copy_(k1_span_slot)
     torch.cuda.synchronize()
-    k1_ms = statistics.mean(e[0].elapsed_time(e[1]) for e in ev)
+    k1_event_ms = statistics.mean(e[0].elapsed_time(e[1]) for e in ev)
+    k1_ms = float((k1_spans[:, 1] - k1_spans[:, 0]).float().mean()) / 1e6
 
     # quantisation error vs fp32 attention over the unquantised K/V (group 0),
     # with the stationary decode token included
@@ -916,8 +929,14 @@ def run_c5(args, cfg):
                    "prefill_tokens_per_step": len(pf_slots), "prefix_groups": ngroups,
                    "l2": "pool %.2f GB; shared prefixes are re-read by 8 sequences (L2 hits expected)"
                          % (cache.nbytes() / 1e9)},
-        "k1_ms": k1_ms, "k2_ms": k2_ms,
+        "k1_ms": k1_ms, "k1_event_ms": k1_event_ms, "k1_in_step_ms": k1_step_ms, "k2_ms": k2_ms,
+        "append_bytes": append_bytes,
         "append_gbs": append_bytes / (k1_ms * 1e-3) / 1e9,
+        "append_frac": append_bytes / (k1_ms * 1e-3) / 1e9 / peak,
+        "k1_time": "k1_ms: grid span of K1 alone (first CTA start to last CTA end, %globaltimer; "
+                   "kvq_profile_next_append), its graph replayed back to back; k1_event_ms: CUDA events "
+                   "around each replay (adds the graph launch); k1_in_step_ms: K1's span inside the timed "
+                   "PDL step graph (K2 streams beside it)",
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": ncu_traffic("c5")[0], "kernel": "kvq::decode_kernel",
                      "algorithmic_bytes_per_launch": attn_unique, "unique_kv_bytes": attn_unique_kv,

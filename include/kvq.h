@@ -40,8 +40,9 @@
 extern "C" {
 #endif
 
-#define KVQ_ABI_VERSION 3 /* 2: peer gather, decode_step (+flags), pipeline submitter, block gather/scatter;
-                             3: kvq_check_device_errors, kvq_profile_next_decode */
+#define KVQ_ABI_VERSION 4 /* 2: peer gather, decode_step (+flags), pipeline submitter, block gather/scatter;
+                             3: kvq_check_device_errors, kvq_profile_next_decode;
+                             4: kvq_profile_next_append */
 #define KVQ_HEAD_DIM 128  /* d */
 #define KVQ_BLOCK_SIZE 16 /* tokens per page */
 #define KVQ_PAGE_BYTES 4224 /* one (block, kv head): 2x16x128 codes + 2x16 fp32 scales */
@@ -80,6 +81,9 @@ int kvq_check_device_errors(void* stream, uint32_t* bits);
  * per captured launch) and the kernel times itself inside a PDL-chained step.
  * NULL cancels a pending request. */
 int kvq_profile_next_decode(uint64_t* span);
+/* The same for the next K1 launch (kvq_quant_append, or the K1 half of
+ * kvq_decode_step*). */
+int kvq_profile_next_append(uint64_t* span);
 
 /* Quantize-on-append (K1).  k, v: bf16 [T][Hkv][128] with token strides
  * k_token_stride / v_token_stride (in elements; head stride is 128, rows

@@ -263,10 +263,11 @@ template <int KVD>
 __global__ void __launch_bounds__(K1T_THREADS, 2) quant_append_tile_kernel(
     const __grid_constant__ CUtensorMap tmk, const __grid_constant__ CUtensorMap tmv,
     const int32_t* __restrict__ slots, int T, int Hkv, uint8_t* __restrict__ pool, int64_t num_blocks,
-    int nunits) {
+    int nunits, unsigned long long* span) {
   // A K2 launched behind this kernel with programmatic serialization may start
   // its prologue now; it waits (griddepcontrol.wait) before reading any page.
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  if (span && threadIdx.x == 0) atomicMin(span, global_ns());
   extern __shared__ __align__(128) uint8_t smem_raw[];
   uint8_t* const smem = smem_raw + ((128 - (smem_u32(smem_raw) & 127)) & 127);  // TMA boxes: 128-byte aligned
   uint8_t* const stage = smem;
@@ -358,6 +359,10 @@ __global__ void __launch_bounds__(K1T_THREADS, 2) quant_append_tile_kernel(
   }
   // the images must stay valid until the bulk copies have read them
   if (issuer) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+  if (span) {  // kvq_profile_next_append: the consumers finish last; CTA end = all teams done
+    asm volatile("bar.sync 5, 256;" ::: "memory");
+    if (ct == 0) atomicMax(span + 1, global_ns());
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -372,13 +377,9 @@ constexpr int K1R_WARPS = 8;
 constexpr int64_t K1_ROWS_MAX = 8192;
 
 template <int KVD>
-__global__ void __launch_bounds__(K1R_WARPS * 32) quant_append_rows_kernel(
-    const __nv_bfloat16* __restrict__ k, const __nv_bfloat16* __restrict__ v, int64_t k_stride,
-    int64_t v_stride, const int32_t* __restrict__ slots, int T, int Hkv,
-    uint8_t* __restrict__ pool, int64_t num_blocks) {
-  // A K2 launched behind this kernel with programmatic serialization may start
-  // its prologue now; it waits (griddepcontrol.wait) before reading any page.
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+__device__ __forceinline__ void quant_row(const __nv_bfloat16* __restrict__ k, const __nv_bfloat16* __restrict__ v,
+                                          int64_t k_stride, int64_t v_stride, const int32_t* __restrict__ slots,
+                                          int T, int Hkv, uint8_t* __restrict__ pool, int64_t num_blocks) {
   const int row = blockIdx.x * K1R_WARPS + (threadIdx.x >> 5);  // t * Hkv + h
   const int lane = threadIdx.x & 31;
   if (row >= T * Hkv) return;  // whole warps only
@@ -417,6 +418,24 @@ __global__ void __launch_bounds__(K1R_WARPS * 32) quant_append_rows_kernel(
   }
 }
 
+template <int KVD>
+__global__ void __launch_bounds__(K1R_WARPS * 32) quant_append_rows_kernel(
+    const __nv_bfloat16* __restrict__ k, const __nv_bfloat16* __restrict__ v, int64_t k_stride,
+    int64_t v_stride, const int32_t* __restrict__ slots, int T, int Hkv,
+    uint8_t* __restrict__ pool, int64_t num_blocks, unsigned long long* span) {
+  // A K2 launched behind this kernel with programmatic serialization may start
+  // its prologue now; it waits (griddepcontrol.wait) before reading any page.
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  if (span) {  // kvq_profile_next_append: CTA start, and CTA end once every warp is done
+    if (threadIdx.x == 0) atomicMin(span, global_ns());
+    quant_row<KVD>(k, v, k_stride, v_stride, slots, T, Hkv, pool, num_blocks);
+    __syncthreads();
+    if (threadIdx.x == 0) atomicMax(span + 1, global_ns());
+    return;
+  }
+  quant_row<KVD>(k, v, k_stride, v_stride, slots, T, Hkv, pool, num_blocks);
+}
+
 unsigned read_and_clear_dev_err_append() { return read_and_clear_dev_err_tu(); }
 
 }  // namespace kvq
@@ -424,6 +443,15 @@ unsigned read_and_clear_dev_err_append() { return read_and_clear_dev_err_tu(); }
 using namespace kvq_abi;
 
 extern "C" {
+
+// kvq_profile_next_append: one-shot span pointer for this host thread's next K1 launch.
+static thread_local unsigned long long* t_next_append_span = nullptr;
+
+int kvq_profile_next_append(uint64_t* span) {
+  if (span && !aligned(span, 8)) return fail(KVQ_EINVAL, "profile_next_append: span must be 8-byte aligned");
+  t_next_append_span = reinterpret_cast<unsigned long long*>(span);
+  return KVQ_OK;
+}
 
 int kvq_quant_append(const void* k, const void* v, int64_t k_token_stride, int64_t v_token_stride,
                      const int32_t* slot_mapping, int32_t T, int32_t Hkv, int32_t kv_dtype,
@@ -438,6 +466,8 @@ int kvq_quant_append(const void* k, const void* v, int64_t k_token_stride, int64
   if (int rc = check_device()) return rc;
   if (Hkv > 65535) return fail(KVQ_EINVAL, "quant_append: Hkv too large");
   auto st = static_cast<cudaStream_t>(stream);
+  unsigned long long* const span = t_next_append_span;
+  t_next_append_span = nullptr;
   // Same (max-shared) L1/smem carveout as K2 so a decode step never pays an
   // SM reconfiguration between the append and the attention kernel.
   static const bool carve = [] {
@@ -462,10 +492,10 @@ int kvq_quant_append(const void* k, const void* v, int64_t k_token_stride, int64
     const unsigned nblk = (unsigned)((T * Hkv + kvq::K1R_WARPS - 1) / kvq::K1R_WARPS);
     if (kv_dtype == KVQ_INT8)
       kvq::quant_append_rows_kernel<KVQ_INT8><<<nblk, kvq::K1R_WARPS * 32, 0, st>>>(
-          kp, vp, k_token_stride, v_token_stride, slot_mapping, T, Hkv, pp, num_blocks);
+          kp, vp, k_token_stride, v_token_stride, slot_mapping, T, Hkv, pp, num_blocks, span);
     else
       kvq::quant_append_rows_kernel<KVQ_FP8_E4M3><<<nblk, kvq::K1R_WARPS * 32, 0, st>>>(
-          kp, vp, k_token_stride, v_token_stride, slot_mapping, T, Hkv, pp, num_blocks);
+          kp, vp, k_token_stride, v_token_stride, slot_mapping, T, Hkv, pp, num_blocks, span);
     return check_launch("quant_append");
   }
   // Tile kernel: the rows are fetched by TMA tensor loads through two maps
@@ -497,10 +527,10 @@ int kvq_quant_append(const void* k, const void* v, int64_t k_token_stride, int64
   const unsigned grid = (unsigned)std::min<int64_t>(nunits, (int64_t)sms * 2);
   if (kv_dtype == KVQ_INT8)
     kvq::quant_append_tile_kernel<KVQ_INT8><<<grid, kvq::K1T_THREADS, kvq::K1T_SMEM, st>>>(
-        maps[0], maps[1], slot_mapping, T, Hkv, pp, num_blocks, (int)nunits);
+        maps[0], maps[1], slot_mapping, T, Hkv, pp, num_blocks, (int)nunits, span);
   else
     kvq::quant_append_tile_kernel<KVQ_FP8_E4M3><<<grid, kvq::K1T_THREADS, kvq::K1T_SMEM, st>>>(
-        maps[0], maps[1], slot_mapping, T, Hkv, pp, num_blocks, (int)nunits);
+        maps[0], maps[1], slot_mapping, T, Hkv, pp, num_blocks, (int)nunits, span);
   return check_launch("quant_append");
 }
 

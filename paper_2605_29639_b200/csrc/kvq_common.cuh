@@ -44,6 +44,12 @@ __host__ __device__ __forceinline__ int v_code_off(int tok, int d) {
   return V_OFF + R * 128 + (((l >> 4) ^ (R & 7)) << 4) + (l & 15);
 }
 
+__device__ __forceinline__ unsigned long long global_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }

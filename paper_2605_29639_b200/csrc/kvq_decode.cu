@@ -98,11 +98,6 @@ __device__ __forceinline__ void st_release_sys(uint32_t* a, uint32_t v) {
 __device__ __forceinline__ void red_add_release_sys(uint32_t* a, uint32_t v) {
   asm volatile("red.release.sys.global.add.u32 [%0], %1;" ::"l"(a), "r"(v) : "memory");
 }
-__device__ __forceinline__ unsigned long long global_ns() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  return t;
-}
 // Spin until (int)(*w - target) >= 0; on timeout set the error word and give up.
 __device__ __noinline__ void spin_until(const uint32_t* w, uint32_t target, uint32_t* err) {
   const unsigned long long t0 = global_ns();

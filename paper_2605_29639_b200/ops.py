@@ -54,6 +54,16 @@ def profile_next_decode(span: Optional[torch.Tensor]) -> None:
                _lib.load().kvq_profile_next_decode(span.data_ptr() if span is not None else None))
 
 
+def profile_next_append(span: Optional[torch.Tensor]) -> None:
+    """The same for this thread's next K1 launch (``kvq_profile_next_append``)."""
+    if span is not None:
+        _require_cuda("profile_next_append", span)
+        if span.dtype not in (torch.int64, torch.uint64) or span.numel() < 2:
+            raise ValueError("profile_next_append: span must hold 2 x 64-bit")
+    _lib.check("kvq_profile_next_append",
+               _lib.load().kvq_profile_next_append(span.data_ptr() if span is not None else None))
+
+
 def _require_cuda(name: str, *ts: torch.Tensor) -> None:
     for t in ts:
         if not t.is_cuda:

@@ -199,12 +199,12 @@ __device__ __forceinline__ uint32_t movmatrix_trans(uint32_t x) {
 template <int S>
 struct PageStream {
   const int32_t* bt;       // block table row, offset to the split's first page
-  const uint8_t* head_base;
-  int64_t blk_stride;
+  uint64_t head_base;      // global address of (block 0, this kv head)
+  uint32_t blk_stride;     // Hkv * PAGE (< 2^28)
   int64_t num_blocks;
   int warp, nj;            // nj = pages this warp processes
-  uint8_t* ring;           // this warp's S slots
-  uint64_t* full;          // this warp's S barriers
+  uint32_t ring_s;         // this warp's S slots (shared-window address)
+  uint32_t full_s;         // this warp's S barriers (shared-window address)
   uint64_t policy;
   int cur, nxt;            // block ids of pages [base, base+32) and [base+32, base+64) (lane-parallel)
   int base;
@@ -225,17 +225,22 @@ struct PageStream {
     nxt = nj > 32 ? load_ids(32, lane) : 0;
   }
   // Issue the bulk copy of page j into slot s (j >= base, all lanes participate).
+  // Addresses: 32-bit shared-window offsets (slot s is a compile-time constant
+  // in the unrolled page loop) and one wide multiply-add for the page's global
+  // address, so the issue path holds few registers and needs no generic ->
+  // shared conversions.
   __device__ __forceinline__ void issue(int j, int lane, int s) {
     if (j >= base + 32) {  // advance the id window (warp-uniform)
       base += 32;
       cur = nxt;
       nxt = load_ids(base + 32, lane);
     }
-    const int blk = __shfl_sync(FULL, cur, j - base);
+    const uint32_t blk = (uint32_t)__shfl_sync(FULL, cur, j - base);
     if (lane == 0) {
       if (j == wait_j) asm volatile("griddepcontrol.wait;" ::: "memory");
-      mbar_arrive_expect_tx(&full[s], PAGE);
-      bulk_g2s(ring + s * PAGE, head_base + blk * blk_stride, PAGE, &full[s], policy);
+      const uint32_t bar = full_s + 8 * s;
+      mbar_arrive_expect_tx_s(bar, PAGE);
+      bulk_g2s_s(ring_s + s * PAGE, head_base + (uint64_t)blk * blk_stride, PAGE, bar, policy);
     }
   }
 };
@@ -304,17 +309,17 @@ __device__ __forceinline__ void decode_cta(const DecodeParams& p, uint8_t* smem)
 
   PageStream<S> ps;
   ps.bt = p.block_table + (int64_t)b * p.max_blocks + pg0;
-  ps.head_base = p.pool + (int64_t)h * PAGE;
-  ps.blk_stride = (int64_t)p.Hkv * PAGE;
+  ps.head_base = reinterpret_cast<uint64_t>(p.pool) + (uint64_t)h * PAGE;
+  ps.blk_stride = (uint32_t)p.Hkv * PAGE;
   ps.num_blocks = p.num_blocks;
   ps.warp = warp;
   ps.nj = n > warp ? (n - warp + NW - 1) / NW : 0;
-  ps.ring = smem + warp * S * PAGE;
-  ps.full = bars + warp * S;
+  ps.ring_s = smem_u32(smem + warp * S * PAGE);
+  ps.full_s = smem_u32(bars + warp * S);
   ps.policy = policy_evict_first();
   if (lane == 0) {
 #pragma unroll
-    for (int s = 0; s < S; ++s) mbar_init(&ps.full[s], 1);
+    for (int s = 0; s < S; ++s) mbar_init(bars + warp * S + s, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncwarp();
@@ -429,6 +434,8 @@ __device__ __forceinline__ void decode_cta(const DecodeParams& p, uint8_t* smem)
       const float s1 = amax > 0.0f ? pow2i(qex - 7) : 0.0f;
       const float inv1 = amax > 0.0f ? pow2i(7 - qex) : 0.0f;
       qscale = p.sm_scale_log2 * s1 * 0.00390625f;  // S = s1 * (256 acc1 + acc2) / 256
+      // g > 8: the fragments go to shared memory once per CTA; warp 0 makes them
+      if (!HI || warp == 0)
 #pragma unroll
       for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
@@ -456,6 +463,7 @@ __device__ __forceinline__ void decode_cta(const DecodeParams& p, uint8_t* smem)
       if (amax > 0.0f) frexpf(amax, &ex);
       const float pre = pow2i(14 - ex);
       qscale = p.sm_scale_log2 / pre;
+      if (!HI || warp == 0)
 #pragma unroll
       for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
@@ -498,7 +506,7 @@ __device__ __forceinline__ void decode_cta(const DecodeParams& p, uint8_t* smem)
   const uint32_t vb0 = V_OFF + (2 * c) * 128 + ((r ^ (2 * c)) << 4);
   const uint32_t vb1 = V_OFF + (2 * c + 1) * 128 + ((r ^ (2 * c + 1)) << 4);
   const uint32_t sb = 4 * r;
-  const uint32_t ring_s = smem_u32(ps.ring);
+  const uint32_t ring_s = ps.ring_s;
 
   // O^T accumulators: o[nt][mt] : c0 = (d = DA, head 2c), c1 = (DA, 2c+1),
   // c2 = (DA+1, 2c), c3 = (DA+1, 2c+1); DA = (mt < 4 ? 8r + 2mt : 64 + 8r + 2(mt-4)).
@@ -525,11 +533,18 @@ __device__ __forceinline__ void decode_cta(const DecodeParams& p, uint8_t* smem)
   const int L_all = L - (qlen - 1);  // tokens visible to every query row
   auto vis = [&](int nt, int e) { return MQ ? L_all + (8 * nt + 2 * c + e) / g : L; };
 
-  int slot = 0;
+  // The page loop is unrolled by the ring depth S, so every slot's shared
+  // addresses (page, barrier) are immediates and the slot / phase counters
+  // vanish (at the g = 16 variant's 128-register cap they had been spilled
+  // and the page addresses rematerialised from SR_TID / SR_CgaCtaId).
   uint32_t phase = 0;
 #pragma unroll 1
-  for (int j = 0; j < ps.nj; ++j) {
-    mbar_wait(&ps.full[slot], phase);
+  for (int j0 = 0; j0 < ps.nj; j0 += S, phase ^= 1) {
+#pragma unroll
+  for (int slot = 0; slot < S; ++slot) {
+    const int j = j0 + slot;
+    if (j >= ps.nj) break;
+    mbar_wait_s(ps.full_s + 8 * slot, phase);
     const uint32_t pgs = ring_s + slot * PAGE;
     if (FUSED && j == patch_j) {  // the new row over the copy's (possibly stale) bytes
       const uint32_t cv = patch[2 * lane + 1];
@@ -567,15 +582,14 @@ __device__ __forceinline__ void decode_cta(const DecodeParams& p, uint8_t* smem)
       const uint32_t kr8[8] = {k0.y, k1.y, k2.y, k3.y, k0.w, k1.w, k2.w, k3.w};
       uint4 qpair[NT];
       if constexpr (KVD == KVQ_INT8) {
-        int acc1[NT][4], acc2[NT][4];
+        // g > 8: one n-tile at a time (its 8 accumulators, then its scores),
+        // so the live set stays under the 128-register cap; g <= 8: k-steps
+        // outer, both n-tiles' chains interleaved.
 #pragma unroll
-        for (int nt = 0; nt < NT; ++nt)
+        for (int nt = 0; nt < NT; ++nt) {
+          int acc1[4] = {0, 0, 0, 0}, acc2[4] = {0, 0, 0, 0};
 #pragma unroll
-          for (int e = 0; e < 4; ++e) acc1[nt][e] = acc2[nt][e] = 0;
-#pragma unroll
-        for (int jj = 0; jj < 4; ++jj) {
-#pragma unroll
-          for (int nt = 0; nt < NT; ++nt) {
+          for (int jj = 0; jj < 4; ++jj) {
             uint32_t t1b0, t1b1, t2b0, t2b1;
             if constexpr (HI) {
               qpair[nt] = lds128(reinterpret_cast<const uint8_t*>(
@@ -585,14 +599,12 @@ __device__ __forceinline__ void decode_cta(const DecodeParams& p, uint8_t* smem)
               t1b0 = qf[nt][2 * jj][0]; t1b1 = qf[nt][2 * jj][1];
               t2b0 = qf[nt][2 * jj + 1][0]; t2b1 = qf[nt][2 * jj + 1][1];
             }
-            mma16832_s8(acc1[nt], kr[jj], kr8[jj], kr[4 + jj], kr8[4 + jj], t1b0, t1b1);
-            mma16832_s8(acc2[nt], kr[jj], kr8[jj], kr[4 + jj], kr8[4 + jj], t2b0, t2b1);
+            mma16832_s8(acc1, kr[jj], kr8[jj], kr[4 + jj], kr8[4 + jj], t1b0, t1b1);
+            mma16832_s8(acc2, kr[jj], kr8[jj], kr[4 + jj], kr8[4 + jj], t2b0, t2b1);
           }
+#pragma unroll
+          for (int e = 0; e < 4; ++e) st[nt][e] = __int2float_rn(acc1[e] * 256 + acc2[e]);
         }
-#pragma unroll
-        for (int nt = 0; nt < NT; ++nt)
-#pragma unroll
-          for (int e = 0; e < 4; ++e) st[nt][e] = __int2float_rn(acc1[nt][e] * 256 + acc2[nt][e]);
       } else {
         float sa[NT][4], sb2[NT][4];
 #pragma unroll
@@ -779,10 +791,7 @@ __device__ __forceinline__ void decode_cta(const DecodeParams& p, uint8_t* smem)
       __syncwarp();
       ps.issue(j + S, lane, slot);
     }
-    if (++slot == S) {
-      slot = 0;
-      phase ^= 1;
-    }
+  }
   }
 
   // ===== CTA merge of the NW warps =====

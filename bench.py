@@ -82,9 +82,10 @@ def cpu_model() -> str:
     return "unknown"
 
 
-def ncu_traffic(config: str):
+def ncu_traffic(config: str, kv: str):
     """dram__bytes_read + write per K2 launch from profiles/ncu_traffic.json,
-    only if that capture measured THIS build (same source hash); else None."""
+    only if that capture measured THIS build (same source hash) and the same
+    KV dtype (the kernel's first template argument: 0 INT8, 1 FP8); else None."""
     from paper_2605_29639_b200._build import source_hash
     tp = REPO / "profiles" / "ncu_traffic.json"
     try:
@@ -92,6 +93,8 @@ def ncu_traffic(config: str):
     except (OSError, ValueError):
         return None, None
     if rec.get("src_hash") != source_hash():
+        return None, rec.get("src_hash")
+    if ("decode_kernel<1" if kv == "fp8_e4m3" else "decode_kernel<0") not in rec.get("kernel", ""):
         return None, rec.get("src_hash")
     return rec.get("dram_bytes_per_launch"), rec.get("src_hash")
 
@@ -553,7 +556,7 @@ def run_ours(args, cfg):
     peak, peak_kind = measured_peak()
     achieved = attn_bytes / (k2_ms * 1e-3) / 1e9
     from paper_2605_29639_b200._build import source_hash
-    traffic, traffic_hash = (ncu_traffic(args.config) if world == 1 else (None, None))
+    traffic, traffic_hash = (ncu_traffic(args.config, cfg["kv"]) if world == 1 else (None, None))
     value = B / (ms_step * 1e-3)
     line = {
         "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
@@ -938,7 +941,7 @@ def run_c5(args, cfg):
                    "around each replay (adds the graph launch); k1_in_step_ms: K1's span inside the timed "
                    "PDL step graph (K2 streams beside it)",
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": ncu_traffic("c5")[0], "kernel": "kvq::decode_kernel",
+                     "frac": achieved / peak, "traffic": ncu_traffic("c5", cfg["kv"])[0], "kernel": "kvq::decode_kernel",
                      "algorithmic_bytes_per_launch": attn_unique, "unique_kv_bytes": attn_unique_kv,
                      "logical_bytes_per_launch": attn_logical,
                      "logical_gbs": attn_logical / (k2_ms * 1e-3) / 1e9,

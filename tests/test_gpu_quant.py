@@ -160,3 +160,40 @@ def test_large_append_alignments(cuda, kv_dtype, aligned16):
     O.quant_append(bf16_bits(k), bf16_bits(v), np.asarray(slots, np.int32), DT[kv_dtype], ref)
     gpu = cache.pool.cpu().numpy()
     assert np.array_equal(gpu, ref), int((gpu != ref).sum())
+
+
+@pytest.mark.parametrize("kv_dtype", ["int8", "fp8_e4m3"])
+@pytest.mark.parametrize("Hkv", [1, 3, 8])
+def test_tile_append_heads_and_unequal_strides(cuda, kv_dtype, Hkv):
+    """The TMA-fed tile kernel describes K and V to the TMA as two 2-D views
+    [T][Hkv * 128] with their own token strides: K and V taken from two
+    buffers of different widths, 1 / 3 / 8 kv heads (one head per work unit),
+    T not a multiple of 16 (the last box is zero-filled past T), whole pages
+    mixed with scattered and skipped tokens -- bit-exact with the oracle."""
+    rng = np.random.default_rng(100 + Hkv)
+    T = K1_ROWS_MAX // Hkv + 37
+    nb = T + 64                      # a scattered token takes a whole block
+    perm = rng.permutation(nb)
+    slots, used = [], 0
+    while len(slots) < T:
+        if rng.random() < 0.8:
+            slots += [int(perm[used]) * 16 + t for t in range(16)]
+        else:
+            slots += [int(perm[used]) * 16 + int(rng.integers(0, 16)), -1]
+        used += 1
+    slots = np.asarray(slots[:T], np.int32)
+    k, v = make_kv(T, Hkv, 51, kind="k"), make_kv(T, Hkv, 52, kind="v")
+    kb = torch.zeros((T, Hkv * 128 + 64), dtype=torch.bfloat16)     # token stride Hkv*128 + 64
+    vb = torch.zeros((T, 2 * Hkv * 128 + 8), dtype=torch.bfloat16)  # token stride 2*Hkv*128 + 8
+    kb[:, 64:] = k.reshape(T, -1)
+    vb[:, 8:8 + Hkv * 128] = v.reshape(T, -1)
+    kbd, vbd = kb.to(cuda), vb.to(cuda)
+    kd = kbd[:, 64:].view(T, Hkv, 128)
+    vd = vbd[:, 8:8 + Hkv * 128].view(T, Hkv, 128)
+    assert kd.stride(0) != vd.stride(0) and kd.data_ptr() % 16 == 0 and vd.data_ptr() % 16 == 0
+    cache = PagedKVCache(KVCacheSpec(Hkv, kv_dtype=kv_dtype), nb, device=cuda)
+    quantize_append(cache, kd, vd, torch.as_tensor(slots, dtype=torch.int32, device=cuda))
+    ref = np.zeros((nb, Hkv, O.PAGE), dtype=np.uint8)
+    O.quant_append(bf16_bits(k), bf16_bits(v), slots, DT[kv_dtype], ref)
+    gpu = cache.pool.cpu().numpy()
+    assert np.array_equal(gpu, ref), int((gpu != ref).sum())

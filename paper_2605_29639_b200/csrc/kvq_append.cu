@@ -465,6 +465,7 @@ int kvq_quant_append(const void* k, const void* v, int64_t k_token_stride, int64
     return fail(KVQ_EUNSUPPORTED, "quant_append: unknown kv dtype");
   if (int rc = check_device()) return rc;
   if (Hkv > 65535) return fail(KVQ_EINVAL, "quant_append: Hkv too large");
+  if ((int64_t)T * Hkv > INT32_MAX / 2) return fail(KVQ_EINVAL, "quant_append: too many (token, head) rows");
   auto st = static_cast<cudaStream_t>(stream);
   unsigned long long* const span = t_next_append_span;
   t_next_append_span = nullptr;
@@ -486,9 +487,31 @@ int kvq_quant_append(const void* k, const void* v, int64_t k_token_stride, int64
   const auto vp = static_cast<const __nv_bfloat16*>(v);
   auto* pp = static_cast<uint8_t*>(pool);
   const bool rows16 = aligned(k, 16) && aligned(v, 16) && (k_token_stride % 8) == 0 && (v_token_stride % 8) == 0;
-  if ((int64_t)T * Hkv <= kvq::K1_ROWS_MAX || !rows16) {
-    // Decode-shaped batch (latency-bound), or rows only 8-byte aligned (the tile
-    // kernels load 16 bytes per lane): one warp per (token, head).
+  // Tile kernel: the rows are fetched by TMA tensor loads through two maps over
+  // the [T][Hkv * 128] K and V views (box = 16 tokens x one head).  Decode-
+  // shaped batches (latency-bound), rows only 8-byte aligned, and views the TMA
+  // cannot describe (e.g. a token stride below the row length) take the
+  // one-warp-per-row kernel instead.
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = [] {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      fn = nullptr;
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }();
+  CUtensorMap maps[2];
+  bool tile = (int64_t)T * Hkv > kvq::K1_ROWS_MAX && rows16 && encode != nullptr;
+  for (int m = 0; m < 2 && tile; ++m) {
+    const cuuint64_t dims[2] = {(cuuint64_t)kvq::HD * Hkv, (cuuint64_t)T};
+    const cuuint64_t strides[1] = {(cuuint64_t)(m ? v_token_stride : k_token_stride) * 2};
+    const cuuint32_t box[2] = {(cuuint32_t)kvq::HD, 16};
+    const cuuint32_t estr[2] = {1, 1};
+    tile = encode(&maps[m], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(m ? v : k), dims, strides, box,
+                  estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+  }
+  if (!tile) {
     const unsigned nblk = (unsigned)((T * Hkv + kvq::K1R_WARPS - 1) / kvq::K1R_WARPS);
     if (kv_dtype == KVQ_INT8)
       kvq::quant_append_rows_kernel<KVQ_INT8><<<nblk, kvq::K1R_WARPS * 32, 0, st>>>(
@@ -498,30 +521,8 @@ int kvq_quant_append(const void* k, const void* v, int64_t k_token_stride, int64
           kp, vp, k_token_stride, v_token_stride, slot_mapping, T, Hkv, pp, num_blocks, span);
     return check_launch("quant_append");
   }
-  // Tile kernel: the rows are fetched by TMA tensor loads through two maps
-  // over the [T][Hkv][128] K and V views (16-byte aligned rows, checked above).
-  static PFN_cuTensorMapEncodeTiled_v12000 encode = [] {
-    void* fn = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
-        q != cudaDriverEntryPointSuccess)
-      fn = nullptr;
-    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
-  }();
-  if (!encode) return fail(KVQ_ECUDA, "quant_append: cuTensorMapEncodeTiled unavailable");
-  CUtensorMap maps[2];
-  for (int m = 0; m < 2; ++m) {  // 2-D view [T][Hkv * 128]: box = 16 tokens x one head
-    const cuuint64_t dims[2] = {(cuuint64_t)kvq::HD * Hkv, (cuuint64_t)T};
-    const cuuint64_t strides[1] = {(cuuint64_t)(m ? v_token_stride : k_token_stride) * 2};
-    const cuuint32_t box[2] = {(cuuint32_t)kvq::HD, 16};
-    const cuuint32_t estr[2] = {1, 1};
-    const CUresult r = encode(&maps[m], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(m ? v : k), dims,
-                              strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (r != CUDA_SUCCESS) return fail(KVQ_EINVAL, "quant_append: cannot describe the k/v rows to the TMA");
-  }
   const int64_t nunits = (int64_t)((T + 15) / 16) * Hkv;
-  if (nunits > INT32_MAX) return fail(KVQ_EINVAL, "quant_append: too many tokens");
+  if (nunits > INT32_MAX / 2) return fail(KVQ_EINVAL, "quant_append: too many tokens");
   int sms = 148, dev = 0;
   if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const unsigned grid = (unsigned)std::min<int64_t>(nunits, (int64_t)sms * 2);

@@ -197,3 +197,20 @@ def test_tile_append_heads_and_unequal_strides(cuda, kv_dtype, Hkv):
     O.quant_append(bf16_bits(k), bf16_bits(v), slots, DT[kv_dtype], ref)
     gpu = cache.pool.cpu().numpy()
     assert np.array_equal(gpu, ref), int((gpu != ref).sum())
+
+
+def test_large_append_overlapping_rows_fall_back(cuda):
+    """A token stride the TMA cannot describe (0: every token reads the same
+    row) still appends, through the one-warp-per-row kernel, bit-exact."""
+    Hkv, T = 8, 2048                     # 16384 (token, head) rows: tile-kernel size
+    row = make_kv(1, Hkv, 61, kind="k")
+    k = row.to(cuda).expand(T, Hkv, 128)
+    v = make_kv(1, Hkv, 62, kind="v").to(cuda).expand(T, Hkv, 128)
+    assert k.stride(0) == 0
+    slots = np.arange(T, dtype=np.int32)
+    nb = T // 16
+    cache = PagedKVCache(KVCacheSpec(Hkv), nb, device=cuda)
+    quantize_append(cache, k, v, torch.as_tensor(slots, device=cuda))
+    ref = np.zeros((nb, Hkv, O.PAGE), dtype=np.uint8)
+    O.quant_append(bf16_bits(k.cpu().contiguous()), bf16_bits(v.cpu().contiguous()), slots, O.INT8, ref)
+    assert np.array_equal(cache.pool.cpu().numpy(), ref)

@@ -537,13 +537,19 @@ __device__ __forceinline__ void decode_cta(const DecodeParams& p, uint8_t* smem)
   // addresses (page, barrier) are immediates and the slot / phase counters
   // vanish (at the g = 16 variant's 128-register cap they had been spilled
   // and the page addresses rematerialised from SR_TID / SR_CgaCtaId).
+  // (Not for the multi-query variant: its larger live set spilled in the
+  // unrolled form, q_len = 4 0.42 -> 0.49 ms; there the slot stays a loop
+  // variable.)
+  constexpr int STEP = MQ ? 1 : S;
   uint32_t phase = 0;
+  int slot_rt = 0;  // MQ: the slot of page j0
 #pragma unroll 1
-  for (int j0 = 0; j0 < ps.nj; j0 += S, phase ^= 1) {
+  for (int j0 = 0; j0 < ps.nj; j0 += STEP) {
 #pragma unroll
-  for (int slot = 0; slot < S; ++slot) {
-    const int j = j0 + slot;
+  for (int sl = 0; sl < STEP; ++sl) {
+    const int j = j0 + sl;
     if (j >= ps.nj) break;
+    const int slot = MQ ? slot_rt : sl;
     mbar_wait_s(ps.full_s + 8 * slot, phase);
     const uint32_t pgs = ring_s + slot * PAGE;
     if (FUSED && j == patch_j) {  // the new row over the copy's (possibly stale) bytes
@@ -792,6 +798,11 @@ __device__ __forceinline__ void decode_cta(const DecodeParams& p, uint8_t* smem)
       ps.issue(j + S, lane, slot);
     }
   }
+    if (MQ) {
+      if (++slot_rt == S) slot_rt = 0, phase ^= 1;
+    } else {
+      phase ^= 1;
+    }
   }
 
   // ===== CTA merge of the NW warps =====

@@ -214,3 +214,32 @@ def test_large_append_overlapping_rows_fall_back(cuda):
     ref = np.zeros((nb, Hkv, O.PAGE), dtype=np.uint8)
     O.quant_append(bf16_bits(k.cpu().contiguous()), bf16_bits(v.cpu().contiguous()), slots, O.INT8, ref)
     assert np.array_equal(cache.pool.cpu().numpy(), ref)
+
+
+@pytest.mark.parametrize("kv_dtype", ["int8", "fp8_e4m3"])
+def test_tile_append_in_cuda_graph(cuda, kv_dtype):
+    """The tile kernel's TMA descriptors are kernel parameters (encoded on the
+    host at launch), so a captured K1 replays against whatever the captured
+    K/V buffers hold at replay time: refill them, replay, bit-exact."""
+    Hkv, T = 8, 1100                                   # 8800 rows: tile kernel
+    nb = T // 16 + 8
+    slots = np.arange(16 * 2, 16 * 2 + T, dtype=np.int32)
+    kd = torch.empty((T, Hkv, 128), dtype=torch.bfloat16, device=cuda)
+    vd = torch.empty_like(kd)
+    sd = torch.as_tensor(slots, device=cuda)
+    cache = PagedKVCache(KVCacheSpec(Hkv, kv_dtype=kv_dtype), nb, device=cuda)
+    kd.copy_(make_kv(T, Hkv, 70, kind="k").to(cuda)); vd.copy_(make_kv(T, Hkv, 71, kind="v").to(cuda))
+    quantize_append(cache, kd, vd, sd)                 # warm-up (lazy init outside the capture)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        quantize_append(cache, kd, vd, sd)
+    for seed in (72, 74):
+        k, v = make_kv(T, Hkv, seed, kind="k"), make_kv(T, Hkv, seed + 1, kind="v")
+        kd.copy_(k.to(cuda)); vd.copy_(v.to(cuda))
+        cache.pool.zero_()
+        g.replay()
+        torch.cuda.synchronize()
+        ref = np.zeros((nb, Hkv, O.PAGE), dtype=np.uint8)
+        O.quant_append(bf16_bits(k), bf16_bits(v), slots, DT[kv_dtype], ref)
+        assert np.array_equal(cache.pool.cpu().numpy(), ref), seed

@@ -243,3 +243,29 @@ def test_tile_append_in_cuda_graph(cuda, kv_dtype):
         ref = np.zeros((nb, Hkv, O.PAGE), dtype=np.uint8)
         O.quant_append(bf16_bits(k), bf16_bits(v), slots, DT[kv_dtype], ref)
         assert np.array_equal(cache.pool.cpu().numpy(), ref), seed
+
+
+@pytest.mark.parametrize("kv_dtype", ["int8", "fp8_e4m3"])
+def test_tile_append_long_ring(cuda, kv_dtype):
+    """A long append: ~110 units per CTA, so every stage of the 8-stage ring
+    and every team's image buffers wrap many times (mbarrier phase flips,
+    double-buffered page images reused) -- pool bytes bit-exact."""
+    Hkv, T = 8, 65536 + 7
+    nb = T // 16 + 300
+    rng = np.random.default_rng(81)
+    perm = rng.permutation(nb)
+    slots, used = [], 0
+    while len(slots) < T:
+        if rng.random() < 0.97:
+            slots += [int(perm[used]) * 16 + t for t in range(16)]
+        else:
+            slots += [int(perm[used]) * 16 + int(rng.integers(0, 16))]
+        used += 1
+    slots = np.asarray(slots[:T], np.int32)
+    k, v = make_kv(T, Hkv, 82, kind="k"), make_kv(T, Hkv, 83, kind="v")
+    cache = PagedKVCache(KVCacheSpec(Hkv, kv_dtype=kv_dtype), nb, device=cuda)
+    quantize_append(cache, k.to(cuda), v.to(cuda), torch.as_tensor(slots, device=cuda))
+    ref = np.zeros((nb, Hkv, O.PAGE), dtype=np.uint8)
+    O.quant_append(bf16_bits(k), bf16_bits(v), slots, DT[kv_dtype], ref)
+    gpu = cache.pool.cpu().numpy()
+    assert np.array_equal(gpu, ref), int((gpu != ref).sum())

@@ -660,7 +660,7 @@ def run_serving(args, cfg):
     v_new = torch.randn((B, Hkv, 128), device=dev, generator=gen).to(torch.bfloat16)
     out = torch.empty((B, Hq, 128), dtype=torch.bfloat16, device=dev)
     total_pages = int(np.ceil((lens + 1) / 16).sum())
-    pps = ops.pages_per_split(B, Hkv, total_pages, max_blocks)
+    pps = ops.pages_per_split(B, Hkv, total_pages, max_blocks, rows=Hq // Hkv)
     ws = torch.zeros(ops.workspace_bytes(B, Hq, Hkv, -(-max_blocks // pps)), dtype=torch.uint8, device=dev)
     compute = torch.cuda.current_stream(dev)
     copy_stream = torch.cuda.Stream(dev)
@@ -837,7 +837,7 @@ def run_c5(args, cfg):
     q = torch.randn((B, Hq, 128), device=dev, generator=gen).to(torch.bfloat16)
     total_pages = int(np.ceil(ctx / 16).sum())
     from paper_2605_29639_b200 import ops
-    pps = ops.pages_per_split(B, Hkv, total_pages, table.shape[1])
+    pps = ops.pages_per_split(B, Hkv, total_pages, table.shape[1], rows=Hq // Hkv)
     ws = torch.zeros(ops.workspace_bytes(B, Hq, Hkv, -(-table.shape[1] // pps)), dtype=torch.uint8, device=dev)
     out = torch.empty((B, Hq, 128), dtype=torch.bfloat16, device=dev)
     dec_k = kv_step[0][len(pf_slots):]

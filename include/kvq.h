@@ -40,9 +40,10 @@
 extern "C" {
 #endif
 
-#define KVQ_ABI_VERSION 4 /* 2: peer gather, decode_step (+flags), pipeline submitter, block gather/scatter;
+#define KVQ_ABI_VERSION 5 /* 2: peer gather, decode_step (+flags), pipeline submitter, block gather/scatter;
                              3: kvq_check_device_errors, kvq_profile_next_decode;
-                             4: kvq_profile_next_append */
+                             4: kvq_profile_next_append;
+                             5: kvq_decode_pages_per_split_rows */
 #define KVQ_HEAD_DIM 128  /* d */
 #define KVQ_BLOCK_SIZE 16 /* tokens per page */
 #define KVQ_PAGE_BYTES 4224 /* one (block, kv head): 2x16x128 codes + 2x16 fp32 scales */
@@ -110,6 +111,12 @@ size_t kvq_decode_workspace_bytes(int32_t B, int32_t Hq, int32_t Hkv, int32_t ma
  * max_splits = ceil(max_blocks / pages_per_split). */
 int32_t kvq_decode_pages_per_split(int32_t B, int32_t Hkv, int64_t total_pages,
                                    int32_t max_blocks);
+/* The same for `rows` query rows per kv head ((Hq / Hkv) * q_len; the call
+ * above assumes <= 8).  More than 8 rows run the two-n-tile variant, whose
+ * split combine costs more per split: equal-length launches of 1-8 waves then
+ * get longer splits (C4 at P = 8: 238 -> 192 us).  ABI 5. */
+int32_t kvq_decode_pages_per_split_rows(int32_t B, int32_t Hkv, int32_t rows, int64_t total_pages,
+                                        int32_t max_blocks);
 
 /* Paged GQA decode attention (K2 + fused split-KV combine).
  *   q:           bf16 [B][Hq][128], batch stride q_batch_stride (elements)

@@ -13,7 +13,7 @@ from pathlib import Path
 
 from ._build import LIB_PATH
 
-ABI_VERSION = 4  # include/kvq.h KVQ_ABI_VERSION
+ABI_VERSION = 5  # include/kvq.h KVQ_ABI_VERSION
 KVQ_OK, KVQ_EINVAL, KVQ_EUNSUPPORTED, KVQ_ECUDA = 0, -1, -2, -3
 KVQ_INT8, KVQ_FP8_E4M3 = 0, 1
 KVQ_OUT_BF16, KVQ_OUT_F32 = 0, 1
@@ -39,6 +39,7 @@ SIGNATURES = {
     "kvq_quant_append": (_c.c_int, [_vp, _vp, _i64, _i64, _vp, _i32, _i32, _i32, _vp, _i64, _vp]),
     "kvq_decode_workspace_bytes": (_sz, [_i32, _i32, _i32, _i32]),
     "kvq_decode_pages_per_split": (_i32, [_i32, _i32, _i64, _i32]),
+    "kvq_decode_pages_per_split_rows": (_i32, [_i32, _i32, _i32, _i64, _i32]),
     "kvq_decode_attn": (_c.c_int, [_vp, _i64, _vp, _i64, _vp, _i32, _vp, _i32, _i32, _i32, _i32,
                                    _f32, _i32, _vp, _sz, _vp, _i32, _i32, _vp]),
     "kvq_decode_attn_mq": (_c.c_int, [_vp, _i64, _i32, _vp, _i64, _vp, _i32, _vp, _i32, _i32, _i32,

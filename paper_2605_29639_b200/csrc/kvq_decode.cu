@@ -1050,6 +1050,11 @@ size_t kvq_decode_workspace_bytes(int32_t B, int32_t Hq, int32_t Hkv, int32_t ma
 }
 
 int32_t kvq_decode_pages_per_split(int32_t B, int32_t Hkv, int64_t total_pages, int32_t max_blocks) {
+  return kvq_decode_pages_per_split_rows(B, Hkv, 8, total_pages, max_blocks);
+}
+
+int32_t kvq_decode_pages_per_split_rows(int32_t B, int32_t Hkv, int32_t rows, int64_t total_pages,
+                                        int32_t max_blocks) {
   // Large launches: uniform splits of <= 128 pages (540 KB of KV per CTA) so the
   // ragged tail is at most one short CTA (512 for equal lengths); as few waves
   // of CTAs_PER_SM x SMs as that allows.  Small launches: a latency cost model.
@@ -1109,8 +1114,35 @@ int32_t kvq_decode_pages_per_split(int32_t B, int32_t Hkv, int64_t total_pages, 
   // (Only for big launches -- >= 8 waves at 128-page splits, e.g. C3 / C4: in the
   // few-wave range the 512 cap left ~1 wave of very long CTAs, B = 32 x 8K
   // 110 us vs 92 us at 128 pages.)
-  const bool uniform = max_blocks > 0 && total_pages * 20 >= (int64_t)B * max_blocks * 19 &&
-                       work >= slots * 128 * 8;
+  const bool equal = max_blocks > 0 && total_pages * 20 >= (int64_t)B * max_blocks * 19;
+  const bool uniform = equal && work >= slots * 128 * 8;
+  if (equal && !uniform && rows > 8) {
+    // g > 8 (two n-tiles, C4's shapes), 1-8 waves at 128-page splits, equal
+    // lengths (C4 at P = 4 / 8: 32-128 long sequences per rank).  Its split
+    // combine is serial per (sequence, kv head) in the last CTA and costs
+    // ~0.75 us per split (fit to tools/ab_decode.py PPS sweeps), so the
+    // 128-page cap costs up to 20 % (C4 at P = 8: 238 us at 111 pages, 192 at
+    // 507).  Pick the split from a wave model instead: full waves at the
+    // all-slots page time, the remainder wave at its own concurrency's,
+    //   t = full * pps * tp(slots) + [rem] pps * tp(rem) + 0.75 us * splits,
+    //   tp(c) = max(c * 4224 B / 6.3 TB/s, 0.33 us).
+    static const int cand[] = {64, 96, 128, 170, 255, 340, 507, 768, 1024, 1536, 2048};
+    const int64_t per = max_blocks, pairs = (int64_t)B * Hkv;
+    auto tp = [](double c) { return std::max(c * 4224.0 / 6.3e6, 0.33); };
+    double best_t = 1e30;
+    int64_t best = std::min<int64_t>(per, 128);
+    for (int c : cand) {
+      if (c > per) break;
+      const int64_t ns = (per + c - 1) / c, pps_eff = (per + ns - 1) / ns, ctas = pairs * ns;
+      const int64_t full = ctas / slots, rem = ctas - full * slots;
+      const double t = full * pps_eff * tp((double)slots) + (rem ? pps_eff * tp((double)rem) : 0.0) + 0.75 * ns;
+      if (t < best_t) {
+        best_t = t;
+        best = pps_eff;
+      }
+    }
+    return (int32_t)std::max<int64_t>(1, best);
+  }
   const int64_t cap = uniform ? 512 : 128;
   const int64_t waves = (work + slots * cap - 1) / (slots * cap);
   int64_t pps = (work + slots * (waves > 0 ? waves : 1) - 1) / (slots * (waves > 0 ? waves : 1));
@@ -1170,7 +1202,7 @@ static int decode_attn_impl(const void* q, int64_t q_batch_stride, int32_t q_len
   if (out_layout != KVQ_OUT_BHD && out_layout != KVQ_OUT_HBD)
     return fail(KVQ_EINVAL, "decode_attn: bad out layout");
   if (pages_per_split <= 0)
-    pages_per_split = kvq_decode_pages_per_split(B, Hkv, (int64_t)B * max_blocks, max_blocks);
+    pages_per_split = kvq_decode_pages_per_split_rows(B, Hkv, (Hq / Hkv) * q_len, (int64_t)B * max_blocks, max_blocks);
   const int max_splits = (max_blocks + pages_per_split - 1) / pages_per_split;
   const int64_t rows = (int64_t)Hq * q_len;  // query rows per sequence
   if (workspace_bytes < kvq_decode_workspace_bytes(B, (int32_t)rows, Hkv, max_splits))

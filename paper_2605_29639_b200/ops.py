@@ -102,8 +102,10 @@ def quantize_append(cache: PagedKVCache, k: torch.Tensor, v: torch.Tensor,
     _lib.check("kvq_quant_append", st)
 
 
-def pages_per_split(batch: int, num_kv_heads: int, total_pages: int, max_blocks: int) -> int:
-    return int(_lib.load().kvq_decode_pages_per_split(batch, num_kv_heads, total_pages, max_blocks))
+def pages_per_split(batch: int, num_kv_heads: int, total_pages: int, max_blocks: int, rows: int = 8) -> int:
+    """Split-KV pages per split (``kvq_decode_pages_per_split_rows``); ``rows``
+    = query rows per kv head, (Hq / Hkv) * q_len."""
+    return int(_lib.load().kvq_decode_pages_per_split_rows(batch, num_kv_heads, rows, total_pages, max_blocks))
 
 
 def workspace_bytes(batch: int, num_q_heads: int, num_kv_heads: int, max_splits: int) -> int:
@@ -190,8 +192,9 @@ def paged_decode_attention(q: torch.Tensor, cache: PagedKVCache, block_table: to
         if pages_per_split is not None or num_splits < 1:
             raise ValueError("paged_decode_attention: give num_splits >= 1 or pages_per_split, not both")
         pages_per_split = -(-max_blocks // int(num_splits))
-    pps = pages_per_split or lib.kvq_decode_pages_per_split(
-        B, spec.num_kv_heads, total_pages if total_pages is not None else B * max_blocks, max_blocks)
+    pps = pages_per_split or lib.kvq_decode_pages_per_split_rows(
+        B, spec.num_kv_heads, Hq // spec.num_kv_heads * q_len,
+        total_pages if total_pages is not None else B * max_blocks, max_blocks)
     max_splits = -(-max_blocks // pps)
     nbytes = lib.kvq_decode_workspace_bytes(B, Hq * q_len, spec.num_kv_heads, max_splits)
     if workspace is None:
@@ -242,8 +245,9 @@ def paged_decode_attention_gathered(q: torch.Tensor, cache: PagedKVCache, block_
         sm_scale = 1.0 / math.sqrt(128)
     lib = _lib.load()
     max_blocks = block_table.shape[1]
-    pps = pages_per_split or lib.kvq_decode_pages_per_split(
-        B, spec.num_kv_heads, total_pages if total_pages is not None else B * max_blocks, max_blocks)
+    pps = pages_per_split or lib.kvq_decode_pages_per_split_rows(
+        B, spec.num_kv_heads, Hq // spec.num_kv_heads,
+        total_pages if total_pages is not None else B * max_blocks, max_blocks)
     max_splits = -(-max_blocks // pps)
     nbytes = lib.kvq_decode_workspace_bytes(B, Hq, spec.num_kv_heads, max_splits)
     if workspace is None:
@@ -326,8 +330,9 @@ def decode_step(cache: PagedKVCache, k: torch.Tensor, v: torch.Tensor, slot_mapp
         sm_scale = 1.0 / math.sqrt(128)
     lib = _lib.load()
     max_blocks = block_table.shape[1]
-    pps = pages_per_split or lib.kvq_decode_pages_per_split(
-        B, spec.num_kv_heads, total_pages if total_pages is not None else B * max_blocks, max_blocks)
+    pps = pages_per_split or lib.kvq_decode_pages_per_split_rows(
+        B, spec.num_kv_heads, Hq // spec.num_kv_heads * q_len,
+        total_pages if total_pages is not None else B * max_blocks, max_blocks)
     max_splits = -(-max_blocks // pps)
     nbytes = lib.kvq_decode_workspace_bytes(B, Hq * q_len, spec.num_kv_heads, max_splits)
     if workspace is None:

@@ -70,8 +70,9 @@ class DecodeSession:
         self.head_major, self.sm_scale, self.out_dtype = head_major, sm_scale, out_dtype
         lib = _lib.load()
         max_blocks = block_table.shape[1]
-        self.pps = int(pages_per_split or lib.kvq_decode_pages_per_split(
-            batch, self.Hkv, total_pages if total_pages is not None else batch * max_blocks, max_blocks))
+        self.pps = int(pages_per_split or lib.kvq_decode_pages_per_split_rows(
+            batch, self.Hkv, num_q_heads // self.Hkv,
+            total_pages if total_pages is not None else batch * max_blocks, max_blocks))
         max_splits = -(-max_blocks // self.pps)
         self.depth = depth
         self.compute = torch.cuda.current_stream(dev)

@@ -18,7 +18,7 @@ def declared_functions():
 
 def test_header_matches_binding():
     names = declared_functions()
-    assert len(names) == 23
+    assert len(names) == 24
     assert set(names) == set(_lib.SIGNATURES)
 
 
@@ -27,7 +27,7 @@ def test_library_exports_every_symbol():
     for name in declared_functions():
         assert hasattr(lib, name), name
     L = _lib.load()
-    assert L.kvq_version() == _lib.ABI_VERSION == 4 and L.kvq_page_bytes() == 4224
+    assert L.kvq_version() == _lib.ABI_VERSION == 5 and L.kvq_page_bytes() == 4224
 
 
 def test_host_only_entry_points():

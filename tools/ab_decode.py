@@ -17,7 +17,7 @@ import sys
 import numpy as np
 import torch
 
-SHAPES = {"r8": (8, 32, 8, "ragged", 0), "r32": (32, 32, 8, "ragged", 0), "r64": (64, 32, 8, "ragged", 0), "r64f_p8": (64, 8, 1, "ragged", 1), "c2_p8": (256, 4, 1, "ragged", 0), "c2_p4": (256, 8, 2, "ragged", 0), "c2_p2": (256, 16, 4, "ragged", 0), "c3_p8": (128, 8, 1, 32768, 1), "b1_8k": (1, 32, 8, 8192, 0), "c2h": (128, 32, 8, "ragged", 0), "c2d": (512, 32, 8, "ragged", 0), "b32_8k": (32, 32, 8, 8192, 0), "b1_128k": (1, 32, 8, 131072, 0), "b64_8k": (64, 32, 8, 8192, 0), "b1_32k": (1, 32, 8, 32768, 0), "b4_8k": (4, 32, 8, 8192, 0), "b32_2k": (32, 32, 8, 2048, 0), "tiny": (1, 32, 8, 15, 0), "b1_2k": (1, 32, 8, 2048, 0), "b8_512": (8, 32, 8, 512, 0), "c2f": (256, 32, 8, "ragged", 1), "c3i": (128, 64, 8, 32768, 0), "c2e": (256, 32, 8, 4352, 0), "c1": (8, 32, 8, 2048, 0), "c2": (256, 32, 8, "ragged", 0), "c3": (128, 64, 8, 32768, 1), "c4": (64, 64, 4, 131072, 0)}
+SHAPES = {"r8": (8, 32, 8, "ragged", 0), "r32": (32, 32, 8, "ragged", 0), "r64": (64, 32, 8, "ragged", 0), "r64f_p8": (64, 8, 1, "ragged", 1), "c2_p8": (256, 4, 1, "ragged", 0), "c2_p4": (256, 8, 2, "ragged", 0), "c2_p2": (256, 16, 4, "ragged", 0), "c3_p8": (128, 8, 1, 32768, 1), "c4_p8": (32, 16, 1, 131072, 0), "g16_b16_32k": (16, 64, 4, 32768, 0), "g16_b8_8k": (8, 64, 4, 8192, 0), "c4_p4": (64, 32, 2, 131072, 0), "b1_8k": (1, 32, 8, 8192, 0), "c2h": (128, 32, 8, "ragged", 0), "c2d": (512, 32, 8, "ragged", 0), "b32_8k": (32, 32, 8, 8192, 0), "b1_128k": (1, 32, 8, 131072, 0), "b64_8k": (64, 32, 8, 8192, 0), "b1_32k": (1, 32, 8, 32768, 0), "b4_8k": (4, 32, 8, 8192, 0), "b32_2k": (32, 32, 8, 2048, 0), "tiny": (1, 32, 8, 15, 0), "b1_2k": (1, 32, 8, 2048, 0), "b8_512": (8, 32, 8, 512, 0), "c2f": (256, 32, 8, "ragged", 1), "c3i": (128, 64, 8, 32768, 0), "c2e": (256, 32, 8, 4352, 0), "c1": (8, 32, 8, 2048, 0), "c2": (256, 32, 8, "ragged", 0), "c3": (128, 64, 8, 32768, 1), "c4": (64, 64, 4, 131072, 0)}
 
 
 def main():
@@ -50,12 +50,15 @@ def main():
         L = ctypes.CDLL(path)
         L.kvq_decode_pages_per_split.restype = ctypes.c_int32
         L.kvq_decode_pages_per_split.argtypes = [ctypes.c_int32, ctypes.c_int32, ctypes.c_int64, ctypes.c_int32]
+        if hasattr(L, "kvq_decode_pages_per_split_rows"):
+            L.kvq_decode_pages_per_split_rows.restype = ctypes.c_int32
+            L.kvq_decode_pages_per_split_rows.argtypes = [ctypes.c_int32] * 3 + [ctypes.c_int64, ctypes.c_int32]
         L.kvq_decode_workspace_bytes.restype = ctypes.c_size_t
         L.kvq_decode_workspace_bytes.argtypes = [ctypes.c_int32] * 4
         vp, i32, i64 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64
         L.kvq_decode_attn.argtypes = [vp, i64, vp, i64, vp, i32, vp, i32, i32, i32, i32, ctypes.c_float, i32,
                                       vp, ctypes.c_size_t, vp, i32, i32, vp]
-        pps = int(os.environ.get("PPS", 0)) or L.kvq_decode_pages_per_split(B, Hkv, NB, mb)
+        pps = int(os.environ.get("PPS", 0)) or (L.kvq_decode_pages_per_split_rows(B, Hkv, Hq // Hkv, NB, mb) if hasattr(L, "kvq_decode_pages_per_split_rows") else L.kvq_decode_pages_per_split(B, Hkv, NB, mb))
         wsb = L.kvq_decode_workspace_bytes(B, Hq, Hkv, -(-mb // pps) * int(os.environ.get("WSX", 1)))
         ws = torch.zeros(wsb, dtype=torch.uint8, device=dev)
 

@@ -17,7 +17,7 @@ import sys
 import numpy as np
 import torch
 
-SHAPES = {"r8": (8, 32, 8, "ragged", 0), "r32": (32, 32, 8, "ragged", 0), "r64": (64, 32, 8, "ragged", 0), "r64f_p8": (64, 8, 1, "ragged", 1), "c2_p8": (256, 4, 1, "ragged", 0), "c2_p4": (256, 8, 2, "ragged", 0), "c2_p2": (256, 16, 4, "ragged", 0), "c3_p8": (128, 8, 1, 32768, 1), "c4_p8": (32, 16, 1, 131072, 0), "c3_p2": (128, 32, 4, 32768, 1), "c3_p4": (128, 16, 2, 32768, 1), "g16_b16_32k": (16, 64, 4, 32768, 0), "g16_b8_8k": (8, 64, 4, 8192, 0), "c4_p4": (64, 32, 2, 131072, 0), "b1_8k": (1, 32, 8, 8192, 0), "c2h": (128, 32, 8, "ragged", 0), "c2d": (512, 32, 8, "ragged", 0), "b32_8k": (32, 32, 8, 8192, 0), "b1_128k": (1, 32, 8, 131072, 0), "b64_8k": (64, 32, 8, 8192, 0), "b1_32k": (1, 32, 8, 32768, 0), "b4_8k": (4, 32, 8, 8192, 0), "b32_2k": (32, 32, 8, 2048, 0), "tiny": (1, 32, 8, 15, 0), "b1_2k": (1, 32, 8, 2048, 0), "b8_512": (8, 32, 8, 512, 0), "c2f": (256, 32, 8, "ragged", 1), "c3i": (128, 64, 8, 32768, 0), "c2e": (256, 32, 8, 4352, 0), "c1": (8, 32, 8, 2048, 0), "c2": (256, 32, 8, "ragged", 0), "c3": (128, 64, 8, 32768, 1), "c4": (64, 64, 4, 131072, 0)}
+SHAPES = {"r8": (8, 32, 8, "ragged", 0), "r32": (32, 32, 8, "ragged", 0), "r64": (64, 32, 8, "ragged", 0), "r64f_p8": (64, 8, 1, "ragged", 1), "c2_p8": (256, 4, 1, "ragged", 0), "c2_p4": (256, 8, 2, "ragged", 0), "c2_p2": (256, 16, 4, "ragged", 0), "c3_p8": (128, 8, 1, 32768, 1), "c4_p8": (32, 16, 1, 131072, 0), "g16_b32_8k": (32, 64, 4, 8192, 0), "g16_b4_32k": (4, 64, 4, 32768, 0), "c3_p2": (128, 32, 4, 32768, 1), "c3_p4": (128, 16, 2, 32768, 1), "g16_b16_32k": (16, 64, 4, 32768, 0), "g16_b8_8k": (8, 64, 4, 8192, 0), "c4_p4": (64, 32, 2, 131072, 0), "b1_8k": (1, 32, 8, 8192, 0), "c2h": (128, 32, 8, "ragged", 0), "c2d": (512, 32, 8, "ragged", 0), "b32_8k": (32, 32, 8, 8192, 0), "b1_128k": (1, 32, 8, 131072, 0), "b64_8k": (64, 32, 8, 8192, 0), "b1_32k": (1, 32, 8, 32768, 0), "b4_8k": (4, 32, 8, 8192, 0), "b32_2k": (32, 32, 8, 2048, 0), "tiny": (1, 32, 8, 15, 0), "b1_2k": (1, 32, 8, 2048, 0), "b8_512": (8, 32, 8, 512, 0), "c2f": (256, 32, 8, "ragged", 1), "c3i": (128, 64, 8, 32768, 0), "c2e": (256, 32, 8, 4352, 0), "c1": (8, 32, 8, 2048, 0), "c2": (256, 32, 8, "ragged", 0), "c3": (128, 64, 8, 32768, 1), "c4": (64, 64, 4, 131072, 0)}
 
 
 def main():

@@ -36,6 +36,16 @@ def test_host_only_entry_points():
     assert 64 < L.kvq_decode_pages_per_split(256, 8, 70400, 513) <= 128
     assert 8 <= L.kvq_decode_pages_per_split(8, 8, 8 * 129, 129) <= 64
     assert L.kvq_decode_pages_per_split(1, 1, 3, 3) == 3
+    # query rows per kv head (ABI 5): <= 8 rows is the call above; > 8 rows,
+    # equal lengths, 1-8 waves: longer splits from the wave + serial-combine
+    # model (148 SMs assumed without a GPU) -- C4 at P = 8 fills one wave
+    # (32 sequences x 18 splits = 576 of 592 CTA slots) instead of 111 pages
+    for args in ((256, 8, 70400, 513), (8, 8, 8 * 129, 129), (128, 1, 128 * 2049, 2049)):
+        assert L.kvq_decode_pages_per_split_rows(args[0], args[1], 8, *args[2:]) == \
+            L.kvq_decode_pages_per_split(*args)
+    assert L.kvq_decode_pages_per_split(32, 1, 32 * 8193, 8193) == 111
+    assert L.kvq_decode_pages_per_split_rows(32, 1, 16, 32 * 8193, 8193) == 456
+    assert L.kvq_decode_pages_per_split_rows(64, 4, 16, 64 * 8193, 8193) == 507   # C4 on one GPU: unchanged
     ws = L.kvq_decode_workspace_bytes(4, 32, 8, 3)
     assert ws >= 4 * 32 * 3 * 129 * 4 + 4 * 8 * 4
 
